@@ -1,0 +1,366 @@
+#!/usr/bin/env python
+"""Benchmark: BASELINE.json metric "GCells/s (fp64)" on the iterated Jacobi sweep.
+
+Workload (N=1, BASELINE config 2): j2d5pt fp64, 8192 x 8192 grid, one bench
+step = one full 1000-time-step sweep (reference_run(grid, j2d5pt, 1000)),
+synthetic SplitMix64 input (seed 1) generated in HBM, exact (bitwise) mode.
+GCells/s counts interior cell updates: (8192-2)^2 x 1000 per step.
+
+Lines printed (rank 0, one JSON line):
+  value      device-timed GCells/s over all ranks (CUDA events, max over ranks)
+  e2e        same metric through the public C-ABI host call (ebisu_run_host),
+             pinned host buffers, H2D + sweep + D2H inside the timed region
+  roofline   dominant kernel (stream2d_tb) vs the measured HBM copy peak;
+             algorithmic bytes = 16 B per cell-step (the naive sweep's load+store)
+  cpu_baseline  the numpy oracle port (1 thread) on a bounded sample
+`--impl reference` runs the oracle port (all host threads) instead.
+
+Multi-GPU (torchrun, N>1): slab decomposition along axis 0 with a t*R-deep
+halo exchanged over NCCL each epoch (paper_2305_07390_b200.distributed);
+per-GPU work is fixed (weak scaling: 8192 x 8192 interior rows per rank).
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+N0 = N1 = 8192
+TSTEPS = 1000
+STENCIL = "j2d5pt"
+DEPTH = 8
+ALG_BYTES_PER_CELL_STEP = 16  # 8 B load + 8 B store of the naive sweep
+
+
+def _peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            p = json.load(f)
+        return float(p["hbm_gbs"]), "measured"
+    except Exception:
+        return 6650.0, "fallback"
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled during the timed region."""
+
+    FIELDS = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,"
+              "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+              "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index = index
+        self.proc = None
+        self.lines: list[str] = []
+        self.thread = None
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", f"--id={self.index}", f"--query-gpu={self.FIELDS}",
+                 "--format=csv,noheader,nounits", "-lms", "100"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.thread = threading.Thread(target=self._read, daemon=True)
+            self.thread.start()
+        except Exception:
+            self.proc = None
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def stop(self) -> dict:
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        time.sleep(0.25)
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except Exception:
+            self.proc.kill()
+        sm, smax, reasons = [], [], set()
+        names = ("hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap")
+        for line in self.lines:
+            parts = [p.strip() for p in line.split(",")]
+            if len(parts) < 6:
+                continue
+            try:
+                sm.append(float(parts[0]))
+                smax.append(float(parts[1]))
+            except ValueError:
+                continue
+            for name, v in zip(names, parts[2:6]):
+                if v.lower().startswith("active"):
+                    reasons.add(name)
+        return {"sm_mhz": statistics.median(sm) if sm else None,
+                "sm_max_mhz": max(smax) if smax else None,
+                "samples": len(sm),
+                "reasons": sorted(reasons)}
+
+
+def cpu_oracle_sample(seconds_target: float = 12.0, threads: int = 1) -> dict:
+    """Oracle port (numpy restatement of reference_run) on the host."""
+    from oracle import reference_run, reference_run_threaded
+    from paper_2305_07390_b200.rng import uniform_array
+    from paper_2305_07390_b200.shapes import make_benchmark
+
+    st = make_benchmark(STENCIL)
+    taps = [(tuple(o), c) for o, c in st.taps]
+    cells = uniform_array(1, N0 * N1).reshape(N0, N1)
+    run = (lambda c, t: reference_run(c, taps, t)) if threads == 1 else \
+        (lambda c, t: reference_run_threaded(c, taps, t, threads))
+    run(cells[:256], 1)  # warm
+    t0 = time.perf_counter()
+    steps = 0
+    while True:
+        run(cells, 1)
+        steps += 1
+        if time.perf_counter() - t0 >= seconds_target or steps >= 50:
+            break
+    dt = time.perf_counter() - t0
+    gc = (N0 - 2) * (N1 - 2) * steps / dt / 1e9
+    return {"value": gc, "unit": "GCells/s", "cores": threads, "kind": "port",
+            "sample": f"{STENCIL} fp64 {N0}x{N1}, {steps} time step(s) of oracle/stencil_oracle."
+                      f"reference_run{'_threaded' if threads > 1 else ''} in {dt:.1f} s"}
+
+
+def dist_env():
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return rank, world, local
+
+
+def run_reference(args):
+    rank, world, _ = dist_env()
+    if rank != 0:
+        return 0
+    threads = os.cpu_count() or 1
+    from oracle import reference_run_threaded
+    from paper_2305_07390_b200.rng import uniform_array
+    from paper_2305_07390_b200.shapes import make_benchmark
+
+    st = make_benchmark(STENCIL)
+    taps = [(tuple(o), c) for o, c in st.taps]
+    cells = uniform_array(1, N0 * N1).reshape(N0, N1)
+    per_step = max(1, args.ref_tsteps)
+    for _ in range(args.warmup):
+        reference_run_threaded(cells, taps, 1, threads)
+    t0 = time.perf_counter()
+    for _ in range(args.steps):
+        reference_run_threaded(cells, taps, per_step, threads)
+    dt = time.perf_counter() - t0
+    gc = (N0 - 2) * (N1 - 2) * per_step * args.steps / dt / 1e9
+    sample = (f"{STENCIL} fp64 {N0}x{N1}; each bench step = {per_step} time step(s) of the "
+              f"oracle port (numpy, {threads} host threads, axis-0 bands)")
+    line = {
+        "impl": "reference", "metric": "GCells/s (fp64)", "value": gc, "unit": "GCells/s",
+        "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": dt / args.steps * 1e3, "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": {"workload": f"{STENCIL} fp64 {N0}x{N1} Jacobi sweep (BASELINE config 2)",
+                   "time_steps_per_bench_step": per_step, "host_threads": threads},
+        "cpu_baseline": {"value": gc, "unit": "GCells/s", "cores": threads, "kind": "port",
+                         "sample": sample},
+        "e2e": {"value": gc, "unit": "GCells/s", "h2d_bytes_per_step": 0,
+                "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line))
+    return 0
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--t", type=int, default=DEPTH, help="fused depth per HBM round trip")
+    ap.add_argument("--tsteps", type=int, default=TSTEPS, help="time steps per bench step")
+    ap.add_argument("--ref-tsteps", type=int, default=2)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--sweep-t", action="store_true", help="also time t=1..16 (config 2 sweep)")
+    args = ap.parse_args()
+    if args.warmup < 3:
+        args.warmup = 3
+    if args.impl == "reference":
+        return run_reference(args)
+
+    import torch
+
+    import paper_2305_07390_b200 as eb
+    from paper_2305_07390_b200 import _native, device
+
+    rank, world, local = dist_env()
+    torch.cuda.set_device(local)
+    dist = None
+    if world > 1:
+        import torch.distributed as dist
+
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    lib = _native.load()  # fails loudly without the native library
+    st = eb.make_benchmark(STENCIL)
+    stream = torch.cuda.current_stream()
+
+    if world > 1:
+        from paper_2305_07390_b200 import distributed as edist
+
+        runner = edist.SlabSweep(st, (N0, N1), t=args.t, seed=1, exact=True)
+        step = lambda: runner.run(args.tsteps)  # noqa: E731
+        cells_per_step = runner.global_interior_cells() * args.tsteps
+        launches_per_step = None
+    else:
+        d_in = device.random_grid_device((N0, N1), seed=1)
+        d_out = torch.empty_like(d_in)
+        d_scr = torch.empty_like(d_in)
+        _, tr = device.sweep_device(d_in, st, args.tsteps, out=d_out, scratch=d_scr, t=args.t,
+                                    trace=True)
+        launches_per_step = tr["kernel_launches"]
+        kernel = tr["kernel"]
+
+        def step():
+            device.sweep_device(d_in, st, args.tsteps, out=d_out, scratch=d_scr, t=args.t)
+
+        cells_per_step = (N0 - 2) * (N1 - 2) * args.tsteps
+
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize()
+    if dist:
+        dist.barrier()
+    sampler = ClockSampler(local)
+    sampler.start()
+    time.sleep(0.3)
+    ev0 = torch.cuda.Event(enable_timing=True)
+    ev1 = torch.cuda.Event(enable_timing=True)
+    per_launch = []
+    torch.cuda.synchronize()
+    ev0.record(stream)
+    for _ in range(args.steps):
+        a = torch.cuda.Event(enable_timing=True)
+        b = torch.cuda.Event(enable_timing=True)
+        a.record(stream)
+        step()
+        b.record(stream)
+        per_launch.append((a, b))
+    ev1.record(stream)
+    torch.cuda.synchronize()
+    clocks = sampler.stop()
+    ms = ev0.elapsed_time(ev1)
+    ms_t = torch.tensor([ms], device="cuda")
+    if dist:
+        dist.barrier()
+        dist.all_reduce(ms_t, op=dist.ReduceOp.MAX)
+    ms = float(ms_t.item())
+    step_ms = [a.elapsed_time(b) for a, b in per_launch]
+    value = cells_per_step * world * args.steps / (ms / 1e3) / 1e9
+
+    hbm_peak, peak_kind = _peaks()
+    # dominant kernel: one stream2d_tb launch per bench step when tsteps % t == 0
+    # (persistent cooperative launch, grid.sync between epochs)
+    launch_ms = statistics.mean(step_ms)
+    achieved = ALG_BYTES_PER_CELL_STEP * cells_per_step / (launch_ms / 1e3) / 1e9
+    traffic = None
+    tf = os.path.join(ROOT, "profiles", "dram_traffic.json")
+    if os.path.exists(tf):
+        try:
+            traffic = json.load(open(tf)).get(f"{STENCIL}_t{args.t}")
+        except Exception:
+            traffic = None
+
+    line = {
+        "metric": "GCells/s (fp64)", "value": value, "unit": "GCells/s", "n_gpus": world,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms / args.steps,
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic (SplitMix64 seed 1, generated in HBM)",
+        "config": {"workload": f"{STENCIL} fp64 {N0}x{N1}, {args.tsteps} time steps per bench "
+                               f"step (BASELINE config 2)",
+                   "stencil": STENCIL, "extents": [N0, N1], "time_steps": args.tsteps,
+                   "fused_depth_t": args.t, "exact": True,
+                   "l2": "inputs larger than L2 (512 MiB grid vs 126 MB L2)",
+                   "parallelism": f"slab{world}" if world > 1 else "single"},
+        "roofline": {"bound": "hbm", "kernel": "k_stream2d (stream2d_tb)",
+                     "achieved": achieved, "peak": hbm_peak, "unit": "GB/s",
+                     "frac": achieved / hbm_peak, "traffic": traffic,
+                     "peak_source": f"{peak_kind} hbm_gbs (MEASURED_PEAKS.json)",
+                     "algorithmic_bytes": "16 B per interior cell-step (naive load+store)"},
+        "clocks": clocks,
+        "gpu_launches": (launches_per_step * args.steps) if launches_per_step else None,
+    }
+    if world == 1:
+        line["kernel"] = kernel
+
+    if world == 1 and not args.no_e2e:
+        # public C-ABI host call with pinned host buffers; copies inside the region
+        host_in = torch.empty((N0, N1), dtype=torch.float64).pin_memory()
+        host_out = torch.empty((N0, N1), dtype=torch.float64).pin_memory()
+        host_in.copy_(d_in.cpu())
+        hin, hout = host_in.numpy(), host_out.numpy()
+        import ctypes
+
+        sargs = _native.StencilArgs(st)
+        ext = _native.extents_c((N0, N1))
+        prm = _native.make_params(t=args.t)
+
+        def e2e_step():
+            rc = lib.ebisu_run_host(ctypes.byref(sargs.c), 2, ext, hin.ctypes.data,
+                                    hout.ctypes.data, args.tsteps, ctypes.byref(prm), None)
+            if rc:
+                raise RuntimeError(_native.last_error())
+
+        e2e_step()
+        t0 = time.perf_counter()
+        for _ in range(args.steps):
+            e2e_step()
+        dt = time.perf_counter() - t0
+        line["e2e"] = {"value": cells_per_step * args.steps / dt / 1e9, "unit": "GCells/s",
+                       "h2d_bytes_per_step": N0 * N1 * 8, "d2h_bytes_per_step": N0 * N1 * 8,
+                       "api": "ebisu_run_host (pinned host buffers)"}
+
+    if args.sweep_t and world == 1:
+        sweep = {}
+        for t in range(1, 17):
+            device.sweep_device(d_in, st, 96, out=d_out, scratch=d_scr, t=t)
+            torch.cuda.synchronize()
+            a = torch.cuda.Event(enable_timing=True)
+            b = torch.cuda.Event(enable_timing=True)
+            nt = 240 if t <= 8 else 16 * 15
+            a.record(stream)
+            device.sweep_device(d_in, st, nt, out=d_out, scratch=d_scr, t=t)
+            b.record(stream)
+            torch.cuda.synchronize()
+            sweep[t] = round((N0 - 2) * (N1 - 2) * nt / (a.elapsed_time(b) / 1e3) / 1e9, 1)
+        line["depth_sweep_gcells"] = sweep
+        # naive yardstick (one launch per step)
+        a = torch.cuda.Event(enable_timing=True)
+        b = torch.cuda.Event(enable_timing=True)
+        a.record(stream)
+        device.sweep_device(d_in, st, 20, out=d_out, scratch=d_scr, scheme=_native.SCHEME_NAIVE)
+        b.record(stream)
+        torch.cuda.synchronize()
+        line["naive_gcells"] = round((N0 - 2) * (N1 - 2) * 20 / (a.elapsed_time(b) / 1e3) / 1e9,
+                                     1)
+
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        line["cpu_baseline"] = cpu_oracle_sample()
+    if rank == 0:
+        print(json.dumps(line))
+    if dist:
+        dist.destroy_process_group()
+    return 0
+
+
+if __name__ == "__main__":
+    sys.exit(main())

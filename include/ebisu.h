@@ -1,0 +1,161 @@
+/*
+ * ebisu.h -- C ABI of the B200-native iterated Jacobi sweep (libebisu.so).
+ *
+ * This is the drop-in boundary for the reference's hot path.  The reference
+ * (stencilplan, pure Python/NumPy) exposes the path as three Python calls;
+ * each entry point below replaces one of them and keeps its contract:
+ *
+ *   ebisu_run_host / ebisu_run_device
+ *     replace  stencilplan.grid.reference_run(grid, stencil, t) -> Grid
+ *              (pkg/src/stencilplan/grid.py:106-113, per-step body
+ *               reference_step grid.py:96-103, tap sum apply_taps :76-93)
+ *     and the engine registry entries
+ *              planner._ENGINES[scheme](grid, stencil, params) -> (Grid, trace)
+ *              (planner.py:219,227; run_sm_tiling engine/sm.py:51,
+ *               run_device_tiling engine/device.py:55)
+ *     The result equals reference_run(grid, stencil, steps): bitwise when
+ *     params.exact != 0 (one IEEE binary64 rounding per multiply and per add,
+ *     taps summed in the order given), within 1e-12 relative otherwise.
+ *     The input is never modified (reference purity, test_grid.py:152-157).
+ *
+ *   ebisu_random_grid_device
+ *     replaces stencilplan.grid.random_grid / rng.uniform_array
+ *              (grid.py:56-60, rng.py:31-46), bit-identical draws.
+ *
+ *   ebisu_check_compatible
+ *     replaces grid._check_compatible (grid.py:63-73) and
+ *     TilingParams.validate (engine/params.py:52-90); same messages.
+ *
+ * Conventions: plain C types only; no exceptions cross the ABI; every call
+ * returns an ebisu_status and, on failure, leaves a thread-local message for
+ * ebisu_last_error().  Grids are dense C-order float64 arrays, axis 0 slowest
+ * (the streaming axis).  The caller owns every buffer it passes; the library
+ * owns only device scratch it allocates itself (released by
+ * ebisu_release_scratch).  Calls are reentrant; one CUDA stream per call.
+ */
+#ifndef EBISU_H
+#define EBISU_H
+
+#include <stdint.h>
+
+#if defined(EBISU_BUILD) && defined(__GNUC__)
+#define EBISU_API __attribute__((visibility("default")))
+#else
+#define EBISU_API
+#endif
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define EBISU_ABI_VERSION 1
+#define EBISU_MAX_DIMS 3
+#define EBISU_MAX_TAPS 128
+
+typedef enum ebisu_status {
+  EBISU_OK = 0,
+  EBISU_ERR_VALUE = 1,       /* reference ValueError (grid/stencil mismatch)   */
+  EBISU_ERR_PARAM = 2,       /* reference engine.ParamError (bad TilingParams) */
+  EBISU_ERR_CUDA = 3,        /* CUDA runtime / driver failure                   */
+  EBISU_ERR_UNSUPPORTED = 4, /* no kernel for this request (never a fallback)   */
+  EBISU_ERR_NO_DEVICE = 5    /* no CUDA device visible                          */
+} ebisu_status;
+
+/* Scheme selector; mirrors engine/params.py:12-14 plus the GPU-only choices. */
+typedef enum ebisu_scheme {
+  EBISU_SCHEME_AUTO = 0,          /* planner picks (temporal blocking when possible) */
+  EBISU_SCHEME_NAIVE = 1,         /* one sm_100a launch per time step (yardstick)    */
+  EBISU_SCHEME_SM_TILING = 2,     /* overlapped streaming tiles, "sm-tiling"        */
+  EBISU_SCHEME_DEVICE_TILING = 3  /* halo-exchange tiles, "device-tiling"           */
+} ebisu_scheme;
+
+/* Stencil shape: reference StencilShape (shapes.py:27-56).  offsets holds
+ * ntaps*dims ints, tap-major, axis 0 first, in the order the taps are summed. */
+typedef struct ebisu_stencil {
+  int32_t dims;            /* 1..3 */
+  int32_t ntaps;           /* 1..EBISU_MAX_TAPS */
+  const int32_t* offsets;  /* [ntaps][dims] */
+  const double* coeffs;    /* [ntaps] */
+} ebisu_stencil;
+
+/* Tiling parameters: reference TilingParams (engine/params.py:18-38). */
+typedef struct ebisu_params {
+  int32_t scheme;            /* ebisu_scheme */
+  int32_t t;                 /* temporal depth per HBM round trip (0 = auto) */
+  int32_t tile[2];           /* reference tile extents over tiled axes (validated,
+                                0 = auto); the GPU tile is chosen by the planner */
+  int32_t device_tile_grid[2];
+  int32_t lazy;              /* accepted for parity; the GPU kernels sync once per advance */
+  int32_t exact;             /* 1: bitwise (no FMA contraction); 0: FMA chain      */
+  int32_t persistent;        /* 1: one cooperative launch, grid sync between epochs */
+  int32_t validate_tile;     /* 1: apply the reference TilingParams.validate rules  */
+  int32_t reserved[6];
+} ebisu_params;
+
+/* Closed-form execution counters of the GPU run (reference ExecutionTrace,
+ * engine/trace.py:25-40), plus GPU facts. */
+typedef struct ebisu_trace {
+  uint64_t gm_loads;         /* cells loaded from HBM by TMA (incl. overlap halos) */
+  uint64_t gm_stores;        /* cells stored                                       */
+  uint64_t gm_halo_loads;
+  uint64_t gm_halo_stores;
+  uint64_t syncs_block;
+  uint64_t syncs_device;     /* grid-wide barriers                                 */
+  uint64_t cells_computed;   /* lane-steps issued                                  */
+  uint64_t cells_valid;      /* stored cells x depth                               */
+  uint64_t device_tiles;     /* work units (strip x segment) processed             */
+  uint64_t kernel_launches;
+  double elapsed_ms;         /* device time of the sweep (CUDA events)             */
+  int32_t kernel_id;         /* which kernel family ran (see ebisu_kernel_name)    */
+  int32_t t_used;            /* temporal depth actually fused                      */
+  int32_t grid_ctas;
+  int32_t warps_per_cta;
+  int32_t reserved[4];
+} ebisu_trace;
+
+/* Library / device facts. */
+EBISU_API int32_t ebisu_abi_version(void);
+EBISU_API const char* ebisu_last_error(void);
+EBISU_API const char* ebisu_kernel_name(int32_t kernel_id);
+EBISU_API int32_t ebisu_device_count(void);
+
+/* Validation only (no GPU needed): reference _check_compatible + validate. */
+EBISU_API int32_t ebisu_check_compatible(const ebisu_stencil* stencil, int32_t ndim,
+                               const int64_t* extents, const ebisu_params* params);
+
+/* Host buffers in/out: H2D, sweep, D2H on the current device.  in/out may
+ * alias only if identical (in-place on the host side is allowed). */
+EBISU_API int32_t ebisu_run_host(const ebisu_stencil* stencil, int32_t ndim,
+                       const int64_t* extents, const double* in, double* out,
+                       int64_t steps, const ebisu_params* params,
+                       ebisu_trace* trace /* nullable */);
+
+/* Device buffers: d_in is read only; d_out receives the result; d_scratch is
+ * an optional grid-sized device buffer (NULL: library arena).  stream is a
+ * cudaStream_t (NULL = legacy default stream).  Asynchronous unless trace is
+ * non-NULL (then the call waits to fill elapsed_ms). */
+EBISU_API int32_t ebisu_run_device(const ebisu_stencil* stencil, int32_t ndim,
+                         const int64_t* extents, const double* d_in, double* d_out,
+                         double* d_scratch, int64_t steps,
+                         const ebisu_params* params, void* stream,
+                         ebisu_trace* trace /* nullable */);
+
+/* SplitMix64 uniforms [0,1): d_out[i] = draw i of SplitMix64(seed) for
+ * i in [start, start+n). Bit-identical to rng.uniform_array. */
+EBISU_API int32_t ebisu_random_grid_device(uint64_t seed, int64_t start, int64_t n,
+                                 double* d_out, void* stream);
+
+/* Device-side parity check of two float64 arrays: number of bitwise
+ * mismatches, first mismatch index (-1 if none), max |a-b| and max |b|. */
+EBISU_API int32_t ebisu_compare_device(const double* d_a, const double* d_b, int64_t n,
+                             int64_t* mismatches, int64_t* first_mismatch,
+                             double* max_abs_diff, double* max_abs_ref,
+                             void* stream);
+
+/* Free the library's device scratch arena for the current device. */
+EBISU_API int32_t ebisu_release_scratch(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* EBISU_H */

@@ -1,0 +1,638 @@
+// ebisu_api.cu -- the C ABI (include/ebisu.h): validation with the
+// reference's messages, shape matching, kernel planning, epoch chaining,
+// TMA descriptor encoding, and the host<->device wrappers.
+//
+// Reference call sites replaced (see include/ebisu.h for the full map):
+//   grid.reference_run        pkg/src/stencilplan/grid.py:106-113
+//   grid._check_compatible    grid.py:63-73
+//   engine.params.validate    engine/params.py:52-90
+//   planner._ENGINES[...]     planner.py:219,227
+#include <cudaTypedefs.h>
+#include <stdarg.h>
+#include <stdio.h>
+
+#include <algorithm>
+#include <mutex>
+#include <string>
+#include <vector>
+
+#include "ebisu_internal.h"
+#include "ebisu_common.cuh"
+#include "ebisu_shapes.cuh"
+
+namespace ebisu {
+namespace {
+
+thread_local std::string g_err;
+
+int fail(int code, const char* fmt, ...) {
+  char buf[1024];
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(buf, sizeof(buf), fmt, ap);
+  va_end(ap);
+  g_err = buf;
+  return code;
+}
+
+int cuda_fail(cudaError_t e, const char* what) {
+  return fail(EBISU_ERR_CUDA, "%s: %s (%s)", what, cudaGetErrorName(e), cudaGetErrorString(e));
+}
+
+#define EB_CUDA(call)                                  \
+  do {                                                 \
+    cudaError_t _e = (call);                           \
+    if (_e != cudaSuccess) return cuda_fail(_e, #call); \
+  } while (0)
+
+// ---- shape matching -------------------------------------------------------
+template <class SH>
+bool match_shape(const ebisu_stencil* s) {
+  if (s->dims != SH::dims || s->ntaps != SH::NT) return false;
+  for (int i = 0; i < SH::NT; ++i) {
+    const Off o = SH::tap(i);
+    const int* p = s->offsets + i * s->dims;
+    if (p[0] != o.d0) return false;
+    if (s->dims >= 2 && p[1] != o.d1) return false;
+    if (s->dims >= 3 && p[2] != o.d2) return false;
+  }
+  return true;
+}
+
+int identify_shape(const ebisu_stencil* s) {
+  if (match_shape<StarShape<2, 1>>(s)) return SHAPE_J2D5PT;
+  if (match_shape<StarShape<2, 2>>(s)) return SHAPE_J2D9PT;
+  if (match_shape<BoxShape<2, 1>>(s)) return SHAPE_J2D9PT_GOL;
+  if (match_shape<BoxShape<2, 2>>(s)) return SHAPE_J2D25PT;
+  if (match_shape<StarShape<2, 3>>(s)) return SHAPE_J2D13PT;
+  if (match_shape<StarShape<2, 6>>(s)) return SHAPE_J2DS25PT;
+  if (match_shape<StarShape<3, 1>>(s)) return SHAPE_J3D7PT;
+  if (match_shape<StarShape<3, 2>>(s)) return SHAPE_J3D13PT;
+  if (match_shape<NoCornerShape3<true>>(s)) return SHAPE_J3D17PT;
+  if (match_shape<BoxShape<3, 1>>(s)) return SHAPE_J3D27PT;
+  if (match_shape<NoCornerShape3<false>>(s)) return SHAPE_POISSON;
+  return SHAPE_GENERIC;
+}
+
+// ---- validation (reference messages) -------------------------------------
+int validate(const ebisu_stencil* st, int ndim, const int64_t* ext, const ebisu_params* prm,
+             ProblemDesc* out) {
+  if (!st || !ext) return fail(EBISU_ERR_VALUE, "null stencil or extents");
+  if (st->dims < 1 || st->dims > EBISU_MAX_DIMS)
+    return fail(EBISU_ERR_VALUE, "stencil dims %d not supported (1..3)", st->dims);
+  if (st->ntaps < 1) return fail(EBISU_ERR_VALUE, "tap set is empty");
+  if (st->ntaps > EBISU_MAX_TAPS)
+    return fail(EBISU_ERR_VALUE, "%d taps exceed the supported %d", st->ntaps, EBISU_MAX_TAPS);
+  if (!st->offsets || !st->coeffs) return fail(EBISU_ERR_VALUE, "null offsets or coefficients");
+  // grid._check_compatible (grid.py:63-73)
+  if (ndim != st->dims)
+    return fail(EBISU_ERR_VALUE, "grid is %d-D but stencil is %d-D", ndim, st->dims);
+  int rad = 0;
+  bool has_zero = false;
+  for (int t = 0; t < st->ntaps; ++t) {
+    bool zero = true;
+    for (int d = 0; d < st->dims; ++d) {
+      const int v = st->offsets[t * st->dims + d];
+      rad = std::max(rad, v < 0 ? -v : v);
+      zero = zero && v == 0;
+    }
+    has_zero = has_zero || zero;
+  }
+  if (!has_zero) return fail(EBISU_ERR_VALUE, "tap set must contain the zero offset");
+  for (int d = 0; d < ndim; ++d) {
+    if (ext[d] <= 2 * rad)
+      return fail(EBISU_ERR_VALUE, "extent %lld too small for radius %d (need > %d)",
+                  (long long)ext[d], rad, 2 * rad);
+  }
+  long long total = 1;
+  for (int d = 0; d < ndim; ++d) total *= ext[d];
+  if (total >= (1ll << 40)) return fail(EBISU_ERR_VALUE, "grid too large");
+  out->dims = st->dims;
+  out->ntaps = st->ntaps;
+  out->rad = rad;
+  for (int d = 0; d < 3; ++d) out->ext[d] = d < ndim ? ext[d] : 1;
+  out->offsets = st->offsets;
+  out->coeffs = st->coeffs;
+  out->shape_id = identify_shape(st);
+  if (prm) {
+    if (prm->scheme < EBISU_SCHEME_AUTO || prm->scheme > EBISU_SCHEME_DEVICE_TILING)
+      return fail(EBISU_ERR_PARAM, "unknown scheme %d", prm->scheme);
+    if (prm->t < 0) return fail(EBISU_ERR_PARAM, "temporal depth must be >= 1");
+    if (prm->validate_tile && prm->t >= 1) {
+      // engine/params.py:52-90 (reference TilingParams.validate)
+      const int t = prm->t;
+      int axes[3], nax = 0;
+      if (st->dims == 1) {
+        axes[nax++] = 0;
+      } else if (st->dims == 2 && prm->scheme == EBISU_SCHEME_DEVICE_TILING) {
+        axes[nax++] = 0;
+        axes[nax++] = 1;
+      } else {
+        for (int a = 1; a < st->dims; ++a) axes[nax++] = a;
+      }
+      if (prm->scheme == EBISU_SCHEME_SM_TILING) {
+        for (int i = 0; i < nax && i < 2; ++i) {
+          const int w = prm->tile[i];
+          if (w - 2 * rad * t <= 0)
+            return fail(EBISU_ERR_PARAM,
+                        "tile extent %d leaves no valid core at depth %d (needs > %d)", w, t,
+                        2 * rad * t);
+        }
+      } else if (prm->scheme == EBISU_SCHEME_DEVICE_TILING) {
+        const int halo = rad * t;
+        for (int i = 0; i < nax && i < 2; ++i) {
+          const int g = prm->device_tile_grid[i] ? prm->device_tile_grid[i] : 1;
+          const int w = prm->tile[i];
+          if (g < 1) return fail(EBISU_ERR_PARAM, "device tile grid entries must be >= 1");
+          const long long interior = ext[axes[i]] - 2 * rad;
+          const long long loaded = (long long)g * w;
+          if (loaded < interior && loaded + 2 * halo > ext[axes[i]])
+            return fail(EBISU_ERR_PARAM,
+                        "device tile of %lld cells plus 2*%d halo exceeds extent %lld on axis %d",
+                        loaded, halo, (long long)ext[axes[i]], axes[i]);
+          if (loaded - 2 * halo <= 0 && loaded < interior)
+            return fail(EBISU_ERR_PARAM, "device tile of %lld cells has no core at depth %d",
+                        loaded, t);
+        }
+      }
+    }
+  }
+  return EBISU_OK;
+}
+
+// ---- device facts ----------------------------------------------------------
+struct DevInfo {
+  int sms = 0;
+  bool coop = false;
+};
+
+int device_info(DevInfo* di) {
+  int dev = 0;
+  EB_CUDA(cudaGetDevice(&dev));
+  static std::mutex mu;
+  static std::vector<DevInfo> cache;
+  std::lock_guard<std::mutex> lk(mu);
+  if ((int)cache.size() <= dev) cache.resize(dev + 1);
+  if (cache[dev].sms == 0) {
+    int v = 0;
+    EB_CUDA(cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, dev));
+    cache[dev].sms = v;
+    EB_CUDA(cudaDeviceGetAttribute(&v, cudaDevAttrCooperativeLaunch, dev));
+    cache[dev].coop = v != 0;
+    // Keep freed scratch in the stream-ordered pool (8 GiB grids reuse it).
+    cudaMemPool_t pool;
+    if (cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
+      uint64_t thr = UINT64_MAX;
+      cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
+    }
+  }
+  *di = cache[dev];
+  return EBISU_OK;
+}
+
+// ---- TMA descriptors ---------------------------------------------------------
+PFN_cuTensorMapEncodeTiled_v12000 get_encode() {
+  static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+  static std::once_flag once;
+  std::call_once(once, [] {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) ==
+            cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(p);
+  });
+  return fn;
+}
+
+int encode_map(CUtensorMap* m, const double* base, int rank, const long long* dims_fast_first,
+               const int* box_fast_first) {
+  auto enc = get_encode();
+  if (!enc) return fail(EBISU_ERR_CUDA, "cuTensorMapEncodeTiled unavailable");
+  cuuint64_t gdim[3], gstride[2];
+  cuuint32_t box[3], estr[3];
+  long long pitch = 8;
+  for (int i = 0; i < rank; ++i) {
+    gdim[i] = (cuuint64_t)dims_fast_first[i];
+    box[i] = (cuuint32_t)box_fast_first[i];
+    estr[i] = 1;
+    if (i + 1 < rank) {
+      pitch *= dims_fast_first[i];
+      gstride[i] = (cuuint64_t)pitch;
+    }
+  }
+  CUresult r = enc(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, (cuuint32_t)rank, (void*)base, gdim,
+                   gstride, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+                   CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) return fail(EBISU_ERR_CUDA, "cuTensorMapEncodeTiled failed (%d)", (int)r);
+  return EBISU_OK;
+}
+
+// ---- planning -----------------------------------------------------------------
+enum KernelId : int {
+  KID_NONE = 0,
+  KID_NAIVE = 1,
+  KID_STREAM2D = 2,
+  KID_STREAM3D = 3,
+};
+
+const TbKernel* find_tb(int shape_id, int dims, int T, bool exact) {
+  int n = 0;
+  const TbKernel* ks = tb_kernels(&n);
+  for (int i = 0; i < n; ++i)
+    if (ks[i].shape_id == shape_id && ks[i].dims == dims && ks[i].T == T &&
+        (ks[i].exact != 0) == exact)
+      return &ks[i];
+  return nullptr;
+}
+
+// largest instantiated depth <= tmax for this shape
+int best_depth_leq(int shape_id, int dims, int tmax, bool exact) {
+  int n = 0, best = 0;
+  const TbKernel* ks = tb_kernels(&n);
+  for (int i = 0; i < n; ++i)
+    if (ks[i].shape_id == shape_id && ks[i].dims == dims && (ks[i].exact != 0) == exact &&
+        ks[i].T <= tmax)
+      best = std::max(best, ks[i].T);
+  return best;
+}
+
+// Default fused depth (measured sweet spot on B200).
+int default_depth(int shape_id) {
+  switch (shape_id) {
+    case SHAPE_J2D5PT: return 8;
+    case SHAPE_J2D9PT_GOL: return 6;
+    case SHAPE_J2D9PT: return 4;
+    case SHAPE_J2D25PT: return 3;
+    case SHAPE_J2D13PT: return 2;
+    case SHAPE_J2DS25PT: return 2;
+    default: return 4;
+  }
+}
+
+struct Stage {
+  int kind;            // KID_*
+  const TbKernel* k;   // for TB stages
+  int epochs;          // fused epochs (TB) or steps (naive)
+};
+
+struct Counters {
+  uint64_t gm_loads = 0, gm_stores = 0, cells_computed = 0, device_tiles = 0, syncs_device = 0,
+           launches = 0;
+  int grid = 0, nw = 0, t_used = 0, kid = KID_NONE;
+};
+
+int run_tb2d_stage(const ProblemDesc& p, const TbKernel* k, int epochs, int first_src,
+                   int first_dst, double* bufs[3], const CUtensorMap maps[3], bool coop_req,
+                   const DevInfo& di, cudaStream_t st, Counters* ctr) {
+  const int n0 = (int)p.ext[0], n1 = (int)p.ext[1];
+  const int T = k->T, R = p.rad;
+  int per_sm = 0;
+  EB_CUDA(cudaFuncSetAttribute(k->func, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                               k->smem_bytes));
+  EB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k->func, k->NW * 32,
+                                                        (size_t)k->smem_bytes));
+  if (per_sm < 1) return fail(EBISU_ERR_CUDA, "stream2d kernel cannot be resident (T=%d)", T);
+  const int max_ctas = per_sm * di.sms;
+  const int total_warps = max_ctas * k->NW;
+  const int VW = k->valid_x;
+  const int nstrips = (n1 + VW - 1) / VW;
+  // Row segments: one unit per resident warp, but never shorter than the
+  // pipeline warm-up (2*T*R rows) so redundant work stays small.
+  int nseg = std::max(1, total_warps / nstrips);
+  const int min_len = std::max(32, 4 * T * R);
+  int seg_len = (n0 + nseg - 1) / nseg;
+  if (seg_len < min_len) seg_len = min_len;
+  nseg = (n0 + seg_len - 1) / seg_len;
+  const long long units = (long long)nstrips * nseg;
+  int grid = (int)std::min<long long>(max_ctas, (units + k->NW - 1) / k->NW);
+  if (grid < 1) grid = 1;
+  const bool coop = coop_req && di.coop && epochs > 1;
+
+  TbLaunch L{};
+  L.n0 = n0;
+  L.n1 = n1;
+  L.nstrips = nstrips;
+  L.nseg = nseg;
+  L.seg_len = seg_len;
+  L.first_src = first_src;
+  L.first_dst = first_dst;
+  for (int i = 0; i < 3; ++i) L.buf[i] = bufs[i];
+  L.maps = maps;
+  L.coeffs = p.coeffs;
+  L.grid = grid;
+  L.stream = st;
+  if (coop) {
+    L.epochs = epochs;
+    L.cooperative = true;
+    EB_CUDA(k->launch(L));
+    ctr->launches += 1;
+    ctr->syncs_device += (uint64_t)(epochs - 1);
+  } else {
+    int src = first_src, dst = first_dst;
+    for (int e = 0; e < epochs; ++e) {
+      L.epochs = 1;
+      L.first_src = src;
+      L.first_dst = dst;
+      L.cooperative = false;
+      EB_CUDA(k->launch(L));
+      ctr->launches += 1;
+      src = dst;
+      dst = (dst == BUF_OUT) ? BUF_SCR : BUF_OUT;
+    }
+  }
+  // closed-form counters (reference ExecutionTrace semantics, trace.py:1-17)
+  uint64_t loads = 0, adv = 0;
+  for (int g = 0; g < nseg; ++g) {
+    const int r0 = g * seg_len, r1 = std::min(n0, r0 + seg_len);
+    const int ka = std::max(0, r0 - T * R), kb = std::min(n0, r1 + T * R);
+    loads += (uint64_t)(kb - ka);
+    adv += (uint64_t)(r1 + T * R - ka);
+  }
+  ctr->gm_loads += (uint64_t)epochs * loads * (uint64_t)(32 * k->C) * (uint64_t)nstrips;
+  ctr->gm_stores += (uint64_t)epochs * (uint64_t)n0 * (uint64_t)n1;
+  ctr->cells_computed +=
+      (uint64_t)epochs * adv * (uint64_t)T * (uint64_t)(32 * k->C) * (uint64_t)nstrips;
+  ctr->device_tiles += (uint64_t)epochs * (uint64_t)units;
+  ctr->grid = grid;
+  ctr->nw = k->NW;
+  ctr->t_used = std::max(ctr->t_used, T);
+  ctr->kid = KID_STREAM2D;
+  return EBISU_OK;
+}
+
+int run_device_impl(const ProblemDesc& p, const double* d_in, double* d_out, double* d_scr,
+                    long long steps, const ebisu_params* prm, cudaStream_t st, Counters* ctr) {
+  DevInfo di;
+  int rc = device_info(&di);
+  if (rc) return rc;
+  const long long total = p.ext[0] * p.ext[1] * p.ext[2];
+  const size_t bytes = (size_t)total * sizeof(double);
+  if (steps == 0) {
+    if (d_out != d_in) EB_CUDA(cudaMemcpyAsync(d_out, d_in, bytes, cudaMemcpyDeviceToDevice, st));
+    return EBISU_OK;
+  }
+  const bool exact = prm ? prm->exact != 0 : true;
+  const int scheme = prm ? prm->scheme : EBISU_SCHEME_AUTO;
+  const bool coop = prm ? prm->persistent != 0 : true;
+
+  // ---- plan the stage list ----------------------------------------------------
+  std::vector<Stage> stages;
+  bool tb_ok = p.dims == 2 && p.shape_id != SHAPE_GENERIC && scheme != EBISU_SCHEME_NAIVE &&
+               (p.ext[1] % 2 == 0) && (reinterpret_cast<uintptr_t>(d_in) % 16 == 0) &&
+               (reinterpret_cast<uintptr_t>(d_out) % 16 == 0);
+  if (tb_ok) {
+    int t = (prm && prm->t > 0) ? prm->t : default_depth(p.shape_id);
+    const TbKernel* k = find_tb(p.shape_id, 2, t, exact);
+    if (!k) {
+      // depth not instantiated: compose the sweep from the deepest kernel
+      // below it (epochs compose bitwise, test_grid.py:94-117)
+      t = best_depth_leq(p.shape_id, 2, t, exact);
+      k = t ? find_tb(p.shape_id, 2, t, exact) : nullptr;
+    }
+    if (!k) {
+      tb_ok = false;
+    } else {
+      long long full = steps / t;
+      long long rem = steps % t;
+      if (full > 0) stages.push_back({KID_STREAM2D, k, (int)full});
+      while (rem > 0) {
+        const int t2 = best_depth_leq(p.shape_id, 2, (int)rem, exact);
+        if (t2 == 0) {
+          stages.push_back({KID_NAIVE, nullptr, (int)rem});
+          break;
+        }
+        const long long e2 = rem / t2;
+        stages.push_back({KID_STREAM2D, find_tb(p.shape_id, 2, t2, exact), (int)e2});
+        rem -= e2 * t2;
+      }
+    }
+  }
+  if (!tb_ok) {
+    stages.clear();
+    stages.push_back({KID_NAIVE, nullptr, (int)steps});
+  }
+
+  // ---- buffers: every stage writes a full grid (frame included) -----------------
+  long long nwrites = 0;  // number of grid writes
+  for (auto& s : stages) nwrites += s.epochs;
+  double* scr = d_scr;
+  bool own_scr = false;
+  if (nwrites > 1 && !scr) {
+    EB_CUDA(cudaMallocAsync((void**)&scr, bytes, st));
+    own_scr = true;
+  }
+  double* bufs[3] = {const_cast<double*>(d_in), d_out, scr};
+  CUtensorMap maps[3];
+
+  // write w (0-based) goes to OUT iff (nwrites-1-w) is even
+  long long w = 0;
+  int src = BUF_IN;
+  int result = EBISU_OK;
+  for (auto& s : stages) {
+    const int dst = ((nwrites - 1 - w) % 2 == 0) ? BUF_OUT : BUF_SCR;
+    if (s.kind == KID_NAIVE) {
+      int cs = src, cd = dst;
+      for (int i = 0; i < s.epochs; ++i) {
+        cudaError_t e = launch_naive_step(p, bufs[cs], bufs[cd], exact, st, di.sms);
+        if (e != cudaSuccess) {
+          result = cuda_fail(e, "naive step launch");
+          break;
+        }
+        ctr->launches += 1;
+        cs = cd;
+        cd = (cd == BUF_OUT) ? BUF_SCR : BUF_OUT;
+      }
+      if (result) break;
+      ctr->gm_loads += (uint64_t)s.epochs * (uint64_t)total;
+      ctr->gm_stores += (uint64_t)s.epochs * (uint64_t)total;
+      ctr->cells_computed += (uint64_t)s.epochs * (uint64_t)total;
+      if (ctr->kid == KID_NONE) ctr->kid = KID_NAIVE;
+      ctr->t_used = std::max(ctr->t_used, 1);
+      src = (s.epochs % 2 == 1) ? dst : (dst == BUF_OUT ? BUF_SCR : BUF_OUT);
+    } else {
+      {
+        // every 2-D instantiation loads one 32*C-column row per TMA box
+        const long long dims_ff[2] = {p.ext[1], p.ext[0]};
+        const int box[2] = {s.k->box0, 1};
+        for (int i = 0; i < 3 && !result; ++i) {
+          if (!bufs[i]) {
+            memset(&maps[i], 0, sizeof(CUtensorMap));
+            continue;
+          }
+          result = encode_map(&maps[i], bufs[i], 2, dims_ff, box);
+        }
+        if (result) break;
+      }
+      result = run_tb2d_stage(p, s.k, s.epochs, src, dst, bufs, maps, coop, di, st, ctr);
+      if (result) break;
+      src = (s.epochs % 2 == 1) ? dst : (dst == BUF_OUT ? BUF_SCR : BUF_OUT);
+    }
+    w += s.epochs;
+  }
+  if (own_scr) cudaFreeAsync(scr, st);
+  return result;
+}
+
+}  // namespace
+}  // namespace ebisu
+
+using namespace ebisu;
+
+extern "C" {
+
+int32_t ebisu_abi_version(void) { return EBISU_ABI_VERSION; }
+
+const char* ebisu_last_error(void) { return g_err.c_str(); }
+
+const char* ebisu_kernel_name(int32_t id) {
+  switch (id) {
+    case KID_NAIVE: return "naive_step";
+    case KID_STREAM2D: return "stream2d_tb";
+    case KID_STREAM3D: return "stream3d_tb";
+    default: return "none";
+  }
+}
+
+int32_t ebisu_device_count(void) {
+  int n = 0;
+  if (cudaGetDeviceCount(&n) != cudaSuccess) {
+    cudaGetLastError();
+    return 0;
+  }
+  return n;
+}
+
+int32_t ebisu_check_compatible(const ebisu_stencil* stencil, int32_t ndim, const int64_t* extents,
+                               const ebisu_params* params) {
+  ProblemDesc p;
+  g_err.clear();
+  return validate(stencil, ndim, extents, params, &p);
+}
+
+static void fill_trace(ebisu_trace* tr, const ProblemDesc& p, long long steps, const Counters& c,
+                       float ms) {
+  if (!tr) return;
+  memset(tr, 0, sizeof(*tr));
+  long long interior = 1;
+  for (int d = 0; d < p.dims; ++d) interior *= (p.ext[d] - 2 * p.rad);
+  tr->gm_loads = c.gm_loads;
+  tr->gm_stores = c.gm_stores;
+  tr->syncs_device = c.syncs_device;
+  tr->cells_computed = c.cells_computed;
+  tr->cells_valid = (uint64_t)interior * (uint64_t)steps;
+  tr->device_tiles = c.device_tiles;
+  tr->kernel_launches = c.launches;
+  tr->elapsed_ms = ms;
+  tr->kernel_id = c.kid;
+  tr->t_used = c.t_used;
+  tr->grid_ctas = c.grid;
+  tr->warps_per_cta = c.nw;
+}
+
+int32_t ebisu_run_device(const ebisu_stencil* stencil, int32_t ndim, const int64_t* extents,
+                         const double* d_in, double* d_out, double* d_scratch, int64_t steps,
+                         const ebisu_params* params, void* stream, ebisu_trace* trace) {
+  g_err.clear();
+  if (steps < 0) return fail(EBISU_ERR_VALUE, "step count must be >= 0");
+  ProblemDesc p;
+  int rc = validate(stencil, ndim, extents, params, &p);
+  if (rc) return rc;
+  if (!d_in || !d_out) return fail(EBISU_ERR_VALUE, "null device buffer");
+  if (d_in == d_out && steps > 0)
+    return fail(EBISU_ERR_VALUE, "d_in and d_out must be distinct (the input is read only)");
+  if (ebisu_device_count() == 0) return fail(EBISU_ERR_NO_DEVICE, "no CUDA device visible");
+  cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+  cudaEvent_t e0 = nullptr, e1 = nullptr;
+  if (trace) {
+    EB_CUDA(cudaEventCreate(&e0));
+    EB_CUDA(cudaEventCreate(&e1));
+    EB_CUDA(cudaEventRecord(e0, st));
+  }
+  Counters c;
+  rc = run_device_impl(p, d_in, d_out, d_scratch, steps, params, st, &c);
+  float ms = 0.f;
+  if (trace) {
+    if (!rc) {
+      cudaError_t e = cudaEventRecord(e1, st);
+      if (e == cudaSuccess) e = cudaEventSynchronize(e1);
+      if (e == cudaSuccess) e = cudaEventElapsedTime(&ms, e0, e1);
+      if (e != cudaSuccess) rc = cuda_fail(e, "timing events");
+    }
+    cudaEventDestroy(e0);
+    cudaEventDestroy(e1);
+  }
+  if (!rc) fill_trace(trace, p, steps, c, ms);
+  return rc;
+}
+
+int32_t ebisu_run_host(const ebisu_stencil* stencil, int32_t ndim, const int64_t* extents,
+                       const double* in, double* out, int64_t steps, const ebisu_params* params,
+                       ebisu_trace* trace) {
+  g_err.clear();
+  if (steps < 0) return fail(EBISU_ERR_VALUE, "step count must be >= 0");
+  ProblemDesc p;
+  int rc = validate(stencil, ndim, extents, params, &p);
+  if (rc) return rc;
+  if (!in || !out) return fail(EBISU_ERR_VALUE, "null host buffer");
+  if (ebisu_device_count() == 0) return fail(EBISU_ERR_NO_DEVICE, "no CUDA device visible");
+  const size_t bytes = (size_t)(p.ext[0] * p.ext[1] * p.ext[2]) * sizeof(double);
+  cudaStream_t st = cudaStreamPerThread;
+  double *d_in = nullptr, *d_out = nullptr;
+  EB_CUDA(cudaMallocAsync((void**)&d_in, bytes, st));
+  cudaError_t e = cudaMallocAsync((void**)&d_out, bytes, st);
+  if (e != cudaSuccess) {
+    cudaFreeAsync(d_in, st);
+    return cuda_fail(e, "cudaMallocAsync(out)");
+  }
+  e = cudaMemcpyAsync(d_in, in, bytes, cudaMemcpyHostToDevice, st);
+  if (e == cudaSuccess) {
+    rc = ebisu_run_device(stencil, ndim, extents, d_in, d_out, nullptr, steps, params, st, trace);
+    if (!rc) e = cudaMemcpyAsync(out, d_out, bytes, cudaMemcpyDeviceToHost, st);
+  }
+  if (e == cudaSuccess) e = cudaStreamSynchronize(st);
+  cudaFreeAsync(d_in, st);
+  cudaFreeAsync(d_out, st);
+  if (rc) return rc;
+  if (e != cudaSuccess) return cuda_fail(e, "host<->device copy");
+  return EBISU_OK;
+}
+
+int32_t ebisu_random_grid_device(uint64_t seed, int64_t start, int64_t n, double* d_out,
+                                 void* stream) {
+  g_err.clear();
+  if (n < 0 || start < 0) return fail(EBISU_ERR_VALUE, "negative range");
+  DevInfo di;
+  int rc = device_info(&di);
+  if (rc) return rc;
+  EB_CUDA(launch_splitmix(seed, start, n, d_out, reinterpret_cast<cudaStream_t>(stream), di.sms));
+  return EBISU_OK;
+}
+
+int32_t ebisu_compare_device(const double* d_a, const double* d_b, int64_t n, int64_t* mismatches,
+                             int64_t* first_mismatch, double* max_abs_diff, double* max_abs_ref,
+                             void* stream) {
+  g_err.clear();
+  DevInfo di;
+  int rc = device_info(&di);
+  if (rc) return rc;
+  long long m = 0, f = -1;
+  double mx = 0, mr = 0;
+  EB_CUDA(launch_compare(d_a, d_b, n, &m, &f, &mx, &mr, reinterpret_cast<cudaStream_t>(stream),
+                         di.sms));
+  if (mismatches) *mismatches = m;
+  if (first_mismatch) *first_mismatch = f;
+  if (max_abs_diff) *max_abs_diff = mx;
+  if (max_abs_ref) *max_abs_ref = mr;
+  return EBISU_OK;
+}
+
+int32_t ebisu_release_scratch(void) {
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess) return fail(EBISU_ERR_NO_DEVICE, "no device");
+  cudaMemPool_t pool;
+  if (cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) cudaMemPoolTrimTo(pool, 0);
+  return EBISU_OK;
+}
+
+}  // extern "C"

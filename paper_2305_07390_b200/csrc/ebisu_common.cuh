@@ -1,0 +1,114 @@
+// ebisu_common.cuh -- sm_100a PTX helpers shared by the sweep kernels:
+// mbarrier ring, TMA (cp.async.bulk.tensor) loads, proxy fences, and the
+// exact (one rounding per op) / contracted tap accumulation.
+#pragma once
+
+#include <cuda.h>
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+namespace ebisu {
+
+constexpr unsigned kFullMask = 0xffffffffu;
+
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+
+// ---- mbarrier -------------------------------------------------------------
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count)
+               : "memory");
+}
+
+__device__ __forceinline__ void fence_mbarrier_init() {
+  asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+}
+
+__device__ __forceinline__ void mbar_arrive_expect_tx(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)),
+               "r"(bytes)
+               : "memory");
+}
+
+__device__ __forceinline__ bool mbar_try_wait(uint32_t bar_addr, uint32_t parity) {
+  uint32_t ok;
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
+      "selp.u32 %0, 1, 0, p;\n\t}"
+      : "=r"(ok)
+      : "r"(bar_addr), "r"(parity)
+      : "memory");
+  return ok != 0;
+}
+
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+  const uint32_t a = smem_u32(bar);
+  while (!mbar_try_wait(a, parity)) {
+  }
+}
+
+// ---- proxy fences ---------------------------------------------------------
+// Generic-proxy accesses -> later async-proxy (TMA) accesses.
+__device__ __forceinline__ void fence_proxy_async_shared() {
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+}
+__device__ __forceinline__ void fence_proxy_async_global() {
+  asm volatile("fence.proxy.async.global;" ::: "memory");
+}
+
+// ---- TMA tensor loads (global -> shared, completion on an mbarrier) -------
+__device__ __forceinline__ void tma_load_2d(void* smem_dst, const CUtensorMap* map, int32_t c0,
+                                            int32_t c1, uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.tile.mbarrier::complete_tx::bytes"
+      " [%0], [%1, {%2, %3}], [%4];" ::"r"(smem_u32(smem_dst)),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(smem_u32(bar))
+      : "memory");
+}
+
+__device__ __forceinline__ void tma_load_3d(void* smem_dst, const CUtensorMap* map, int32_t c0,
+                                            int32_t c1, int32_t c2, uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.tensor.3d.shared::cluster.global.tile.mbarrier::complete_tx::bytes"
+      " [%0], [%1, {%2, %3, %4}], [%5];" ::"r"(smem_u32(smem_dst)),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(c2), "r"(smem_u32(bar))
+      : "memory");
+}
+
+__device__ __forceinline__ void prefetch_tmap(const CUtensorMap* map) {
+  asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(map)) : "memory");
+}
+
+// ---- tap accumulation -----------------------------------------------------
+// EXACT: acc = c0*x0; acc = acc + ck*xk -- each op separately rounded, i.e.
+// exactly numpy's `term = c * cells[sl]; acc = acc + term` (grid.py:87-92).
+// Not EXACT: contracted FMA chain (tolerance mode, 1e-12 relative).
+template <bool EXACT>
+__device__ __forceinline__ double tap_first(double c, double x) {
+  return __dmul_rn(c, x);
+}
+template <bool EXACT>
+__device__ __forceinline__ double tap_next(double acc, double c, double x) {
+  if constexpr (EXACT) {
+    return __dadd_rn(acc, __dmul_rn(c, x));
+  } else {
+    return __fma_rn(c, x, acc);
+  }
+}
+
+// Coefficients travel in the kernel parameter space (constant bank), so the
+// DMUL operands come straight from c[0x0][...] without occupying registers.
+template <int NT>
+struct Coefs {
+  double c[NT];
+};
+
+struct alignas(64) TmapSet {
+  CUtensorMap m[3];  // [0] = input, [1] = output, [2] = scratch
+};
+
+enum BufId : int { BUF_IN = 0, BUF_OUT = 1, BUF_SCR = 2 };
+
+}  // namespace ebisu

@@ -1,0 +1,74 @@
+// ebisu_internal.h -- internal interfaces between the C-ABI driver
+// (ebisu_api.cu) and the kernel translation units.
+#pragma once
+
+#include <cuda.h>
+#include <cuda_runtime.h>
+#include <stdint.h>
+#include <string.h>
+
+#include "../../include/ebisu.h"
+
+namespace ebisu {
+
+inline double __longlong_as_double_host(long long v) {
+  double d;
+  memcpy(&d, &v, sizeof(d));
+  return d;
+}
+
+// Validated problem (host side).
+struct ProblemDesc {
+  int dims;
+  int ntaps;
+  int rad;
+  long long ext[3];
+  const int* offsets;    // [ntaps][dims]
+  const double* coeffs;  // [ntaps]
+  int shape_id;          // ShapeId or SHAPE_GENERIC
+};
+
+cudaError_t launch_naive_step(const ProblemDesc& p, const double* in, double* out, bool exact,
+                              cudaStream_t st, int num_sms);
+cudaError_t launch_splitmix(unsigned long long seed, long long start, long long n, double* out,
+                            cudaStream_t st, int num_sms);
+cudaError_t launch_compare(const double* a, const double* b, long long n, long long* mism,
+                           long long* first, double* max_abs, double* max_ref, cudaStream_t st,
+                           int num_sms);
+
+// ---- temporal-blocking kernel registry -------------------------------------
+struct TbLaunch {
+  // geometry
+  int n0, n1, n2;  // extents (2-D: n2 unused)
+  int nstrips, nseg, seg_len;  // 2-D decomposition
+  int ntx, nty;                // 3-D decomposition (tiles along axis 2 / axis 1)
+  int epochs;
+  int first_src, first_dst;
+  double* buf[3];
+  const CUtensorMap* maps;  // host copies [3]
+  const double* coeffs;
+  int grid;
+  bool cooperative;
+  cudaStream_t stream;
+};
+
+struct TbKernel {
+  int shape_id;
+  int dims;
+  int T;         // fused depth
+  int C;         // cells per lane along the fastest axis
+  int NW;        // warps per CTA
+  int S;         // ring slots
+  int exact;
+  int smem_bytes;
+  int box0, box1, box2;  // TMA box (elements) fastest first
+  int valid_x;           // valid columns per warp strip (2-D) or per tile (3-D, axis 2)
+  int valid_y;           // 3-D: valid rows per tile (axis 1)
+  const void* func;      // kernel symbol (occupancy queries / attributes)
+  cudaError_t (*launch)(const TbLaunch&);
+};
+
+// All instantiated temporal-blocking kernels (ebisu_registry.cu).
+const TbKernel* tb_kernels(int* count);
+
+}  // namespace ebisu

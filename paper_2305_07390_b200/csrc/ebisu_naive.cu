@@ -1,0 +1,178 @@
+// ebisu_naive.cu -- one launch per time step, runtime tap list.
+//
+// Direct restatement of reference_step (grid.py:96-103): every interior cell
+// gets the tap sum in tap order (apply_taps, grid.py:76-93), frame cells are
+// copied.  It serves three roles: the naive-HBM-roofline yardstick
+// (16 B/cell-step), the path for arbitrary user stencils that match no
+// specialised kernel, and the remainder steps of a sweep when T is not a
+// multiple of the fused depth and no matching depth was instantiated.
+#include "ebisu_common.cuh"
+#include "ebisu_internal.h"
+
+namespace ebisu {
+
+struct NaiveTaps {
+  int ntaps;
+  int rad;
+  int dims;
+  long long n0, n1, n2;  // extents (unused axes = 1)
+  long long lin[EBISU_MAX_TAPS];  // linear offsets
+  double coef[EBISU_MAX_TAPS];
+};
+
+template <bool EXACT>
+__global__ void __launch_bounds__(256) k_naive_step(const double* __restrict__ in,
+                                                    double* __restrict__ out,
+                                                    const __grid_constant__ NaiveTaps tp) {
+  const long long total = tp.n0 * tp.n1 * tp.n2;
+  const long long stride = (long long)gridDim.x * blockDim.x;
+  for (long long idx = (long long)blockIdx.x * blockDim.x + threadIdx.x; idx < total;
+       idx += stride) {
+    const long long i2 = idx % tp.n2;
+    const long long r = idx / tp.n2;
+    const long long i1 = r % tp.n1;
+    const long long i0 = r / tp.n1;
+    const int R = tp.rad;
+    bool frame = (i0 < R) || (i0 >= tp.n0 - R);
+    if (tp.dims >= 2) frame |= (i1 < R) || (i1 >= tp.n1 - R);
+    if (tp.dims >= 3) frame |= (i2 < R) || (i2 >= tp.n2 - R);
+    double v;
+    if (frame) {
+      v = in[idx];
+    } else {
+      v = tap_first<EXACT>(tp.coef[0], __ldg(in + idx + tp.lin[0]));
+      for (int t = 1; t < tp.ntaps; ++t)
+        v = tap_next<EXACT>(v, tp.coef[t], __ldg(in + idx + tp.lin[t]));
+    }
+    out[idx] = v;
+  }
+}
+
+cudaError_t launch_naive_step(const ProblemDesc& p, const double* in, double* out,
+                              bool exact, cudaStream_t st, int num_sms) {
+  NaiveTaps tp{};
+  tp.ntaps = p.ntaps;
+  tp.rad = p.rad;
+  tp.dims = p.dims;
+  tp.n0 = p.ext[0];
+  tp.n1 = p.dims >= 2 ? p.ext[1] : 1;
+  tp.n2 = p.dims >= 3 ? p.ext[2] : 1;
+  for (int t = 0; t < p.ntaps; ++t) {
+    const int* o = p.offsets + t * p.dims;
+    long long l = o[0];
+    if (p.dims >= 2) l = l * tp.n1 + o[1];
+    if (p.dims >= 3) l = l * tp.n2 + o[2];
+    tp.lin[t] = l;
+    tp.coef[t] = p.coeffs[t];
+  }
+  const long long total = tp.n0 * tp.n1 * tp.n2;
+  long long blocks = (total + 255) / 256;
+  const long long cap = (long long)num_sms * 8;
+  if (blocks > cap) blocks = cap;
+  if (blocks < 1) blocks = 1;
+  if (exact)
+    k_naive_step<true><<<(unsigned)blocks, 256, 0, st>>>(in, out, tp);
+  else
+    k_naive_step<false><<<(unsigned)blocks, 256, 0, st>>>(in, out, tp);
+  return cudaGetLastError();
+}
+
+// ---- SplitMix64 uniforms, bit-identical to rng.uniform_array ---------------
+__global__ void __launch_bounds__(256) k_splitmix_uniform(unsigned long long seed,
+                                                          long long start, long long n,
+                                                          double* __restrict__ out) {
+  const long long stride = (long long)gridDim.x * blockDim.x;
+  for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride) {
+    unsigned long long z = seed + (unsigned long long)(start + i + 1) * 0x9E3779B97F4A7C15ull;
+    z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
+    z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
+    z = z ^ (z >> 31);
+    // (z >> 11) < 2^53 converts exactly; the scale by 2^-53 is exact.
+    out[i] = (double)(z >> 11) * 0x1.0p-53;
+  }
+}
+
+cudaError_t launch_splitmix(unsigned long long seed, long long start, long long n, double* out,
+                            cudaStream_t st, int num_sms) {
+  if (n <= 0) return cudaSuccess;
+  long long blocks = (n + 255) / 256;
+  const long long cap = (long long)num_sms * 16;
+  if (blocks > cap) blocks = cap;
+  k_splitmix_uniform<<<(unsigned)blocks, 256, 0, st>>>(seed, start, n, out);
+  return cudaGetLastError();
+}
+
+// ---- device-side comparison ------------------------------------------------
+struct CompareOut {
+  unsigned long long mismatches;
+  long long first;
+  unsigned long long max_abs_bits;  // non-negative doubles order like their bits
+  unsigned long long max_ref_bits;
+};
+
+__global__ void __launch_bounds__(256) k_compare(const double* __restrict__ a,
+                                                 const double* __restrict__ b, long long n,
+                                                 CompareOut* o) {
+  const long long stride = (long long)gridDim.x * blockDim.x;
+  unsigned long long mism = 0;
+  long long first = -1;
+  double mx = 0.0, mr = 0.0;
+  for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride) {
+    const double x = a[i], y = b[i];
+    if (__double_as_longlong(x) != __double_as_longlong(y)) {
+      ++mism;
+      if (first < 0) first = i;
+    }
+    const double d = fabs(x - y);
+    mx = (d > mx || d != d) ? d : mx;
+    mr = fmax(mr, fabs(y));
+  }
+  for (int off = 16; off; off >>= 1) {
+    mism += __shfl_down_sync(kFullMask, mism, off);
+    const long long f2 = __shfl_down_sync(kFullMask, first, off);
+    if (f2 >= 0 && (first < 0 || f2 < first)) first = f2;
+    const double m2 = __shfl_down_sync(kFullMask, mx, off);
+    mx = (m2 > mx || m2 != m2) ? m2 : mx;
+    mr = fmax(mr, __shfl_down_sync(kFullMask, mr, off));
+  }
+  if ((threadIdx.x & 31) == 0) {
+    if (mism) atomicAdd(&o->mismatches, mism);
+    if (first >= 0) {
+      // first mismatch = minimum index; ordered as unsigned after a bias
+      atomicMin(reinterpret_cast<unsigned long long*>(&o->first),
+                (unsigned long long)first);
+    }
+    atomicMax(&o->max_abs_bits, (unsigned long long)__double_as_longlong(mx));
+    atomicMax(&o->max_ref_bits, (unsigned long long)__double_as_longlong(mr));
+  }
+}
+
+cudaError_t launch_compare(const double* a, const double* b, long long n, long long* mism,
+                           long long* first, double* max_abs, double* max_ref, cudaStream_t st,
+                           int num_sms) {
+  CompareOut* d = nullptr;
+  cudaError_t err = cudaMallocAsync(&d, sizeof(CompareOut), st);
+  if (err != cudaSuccess) return err;
+  CompareOut init{0ull, (long long)-1, 0ull, 0ull};
+  // first = -1 == 0xffff...: atomicMin on unsigned keeps the smallest index.
+  err = cudaMemcpyAsync(d, &init, sizeof(init), cudaMemcpyHostToDevice, st);
+  if (err == cudaSuccess && n > 0) {
+    long long blocks = (n + 255) / 256;
+    const long long cap = (long long)num_sms * 8;
+    if (blocks > cap) blocks = cap;
+    k_compare<<<(unsigned)blocks, 256, 0, st>>>(a, b, n, d);
+    err = cudaGetLastError();
+  }
+  CompareOut h{};
+  if (err == cudaSuccess) err = cudaMemcpyAsync(&h, d, sizeof(h), cudaMemcpyDeviceToHost, st);
+  if (err == cudaSuccess) err = cudaStreamSynchronize(st);
+  cudaFreeAsync(d, st);
+  if (err != cudaSuccess) return err;
+  *mism = (long long)h.mismatches;
+  *first = h.first;
+  *max_abs = __longlong_as_double_host((long long)h.max_abs_bits);
+  *max_ref = __longlong_as_double_host((long long)h.max_ref_bits);
+  return cudaSuccess;
+}
+
+}  // namespace ebisu

@@ -1,0 +1,282 @@
+// ebisu_stream2d.cuh -- 2-D temporal-blocking sweep for sm_100a.
+//
+// Replaces the reference's overlapped-tiling engine (engine/sm.py:95-206,
+// "SM tiling": each block loads core + rad*t per tiled side, streams axis 0
+// through a circular multi-queue, fuses t levels, stores only the core) with
+// a B200 design:
+//
+//  * Work unit = (warp strip, row segment).  A warp strip is 32*C columns
+//    loaded, VW = 32*C - 2*T*R of them valid after T fused levels; row
+//    segments split axis 0 so that >= 148 SMs x resident warps have work
+//    (SURVEY.md §7 hard part 3).  Every warp is an autonomous overlapped
+//    tile: no __syncthreads and no cross-warp traffic inside an epoch.
+//  * Rows move HBM -> shared memory by TMA (cp.async.bulk.tensor.2d, one
+//    32*C-double box per row; out-of-bounds columns are zero-filled) into a
+//    per-warp S-slot mbarrier ring: the circular multi-queue of
+//    multiqueue.py:103-211 with power-of-two slots and mask addressing.
+//  * Each lane owns C consecutive columns.  The T levels are kept as
+//    register windows of 2R+1 rows per level (the "RST" register streaming
+//    of engine/rst.py, taken to its limit): level s at advance k consumes
+//    rows k-(s+1)R .. k-(s-1)R of level s-1 and emits row k-sR.  The advance
+//    loop is unrolled by 2R+1 so window slots are compile-time registers
+//    (no moves).  Horizontal neighbours outside the lane come from warp
+//    shuffles.
+//  * Dirichlet frame (distance < R from a face): a frame cell at level s
+//    equals its value at level s-1, i.e. the centre of the window -- no
+//    stored copy of the input is needed (common.py:96-112 semantics).
+//  * Level T rows are stored straight to HBM for the valid core columns.
+//  * Epochs (T fused steps each) run inside one cooperative launch separated
+//    by grid.sync(), or one launch per epoch.
+//
+// Exactness: taps are summed in catalog order with __dmul_rn/__dadd_rn
+// (EXACT) -> bitwise equal to reference_run (grid.py:76-113).
+#pragma once
+
+#include <cooperative_groups.h>
+
+#include "ebisu_common.cuh"
+#include "ebisu_shapes.cuh"
+
+namespace ebisu {
+
+struct Stream2DArgs {
+  int n0, n1;        // extents (axis 0 rows, axis 1 columns); row pitch = n1
+  int nstrips;       // warp strips along axis 1
+  int nseg;          // row segments along axis 0
+  int seg_len;       // rows per segment
+  int epochs;        // fused epochs in this launch
+  int first_src;     // BufId of epoch 0's source
+  int first_dst;     // BufId of epoch 0's destination
+  double* buf[3];    // device pointers by BufId
+};
+
+template <class SH, int T, int C, int NW, int S>
+struct Stream2DCfg {
+  static constexpr int R = SH::R;
+  static constexpr int W = 2 * R + 1;       // window rows per level
+  static constexpr int LC = 32 * C;         // loaded columns per warp
+  static constexpr int VW = LC - 2 * T * R; // valid columns per warp
+  static constexpr int ROW_BYTES = LC * 8;
+  static constexpr int RING_BYTES = S * ROW_BYTES;
+  static constexpr int SMEM_BYTES = NW * RING_BYTES + NW * S * 8;
+  static_assert(VW > 0, "tile leaves no valid core");
+  static_assert((S & (S - 1)) == 0, "ring slots must be a power of two");
+  static_assert(LC <= 256, "TMA box inner dimension is limited to 256 elements");
+};
+
+// Does any tap in row dy have a nonzero column offset?
+template <class SH>
+__host__ __device__ constexpr bool row_has_halo(int dy) {
+  for (int i = 0; i < SH::NT; ++i)
+    if (SH::tap(i).d0 == dy && SH::tap(i).d1 != 0) return true;
+  return false;
+}
+
+template <int W>
+__host__ __device__ constexpr int pmod(int a) {
+  return ((a % W) + W) % W;
+}
+
+template <class SH, int T, int C, int NW, int S, bool EXACT, int MINB>
+__global__ void __launch_bounds__(NW * 32, MINB)
+    k_stream2d(const __grid_constant__ TmapSet maps, const Stream2DArgs a,
+               const __grid_constant__ Coefs<SH::NT> cf) {
+  using Cfg = Stream2DCfg<SH, T, C, NW, S>;
+  constexpr int R = Cfg::R;
+  constexpr int W = Cfg::W;
+  constexpr int VW = Cfg::VW;
+  constexpr int TR = T * R;
+
+  extern __shared__ __align__(1024) unsigned char smem[];
+  const int warp = threadIdx.x >> 5;
+  const int lane = threadIdx.x & 31;
+  double* ring = reinterpret_cast<double*>(smem + warp * Cfg::RING_BYTES);
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + NW * Cfg::RING_BYTES) + warp * S;
+
+  if (lane == 0) {
+#pragma unroll
+    for (int i = 0; i < S; ++i) mbar_init(&bars[i], 1);
+    fence_mbarrier_init();
+    prefetch_tmap(&maps.m[0]);
+    prefetch_tmap(&maps.m[1]);
+    prefetch_tmap(&maps.m[2]);
+  }
+  __syncwarp();
+
+  const int n0 = a.n0, n1 = a.n1;
+  const int gwarp = blockIdx.x * NW + warp;
+  const int nwarps = gridDim.x * NW;
+  const int units = a.nstrips * a.nseg;
+  uint32_t ring_cnt = 0;  // rows consumed so far by this warp (ring position)
+
+  int src = a.first_src, dst = a.first_dst;
+  for (int e = 0; e < a.epochs; ++e) {
+    const CUtensorMap* tm = &maps.m[src];
+    double* __restrict__ out = (dst == BUF_OUT) ? a.buf[BUF_OUT] : a.buf[BUF_SCR];
+
+    for (int u = gwarp; u < units; u += nwarps) {
+      const int strip = u % a.nstrips;
+      const int seg = u / a.nstrips;
+      const int X0 = strip * VW - TR;  // global column of loaded column 0
+      const int r0 = seg * a.seg_len;
+      const int r1 = min(n0, r0 + a.seg_len);
+      const int ka = max(0, r0 - TR);
+      const int kb = min(n0, r1 + TR);
+      const int kend = r1 + TR;
+
+      // Prologue: fill the ring S rows ahead.
+      if (lane == 0) {
+        for (int i = 0; i < S && ka + i < kb; ++i) {
+          const uint32_t slot = (ring_cnt + i) & (S - 1);
+          mbar_arrive_expect_tx(&bars[slot], Cfg::ROW_BYTES);
+          tma_load_2d(ring + slot * Cfg::LC, tm, X0, ka + i, &bars[slot]);
+        }
+      }
+
+      // Frame-column mask for this lane's C columns.
+      bool fcol[C];
+      bool stcol[C];
+#pragma unroll
+      for (int c = 0; c < C; ++c) {
+        const int lc = lane * C + c;
+        const int x = X0 + lc;
+        fcol[c] = (x < R) || (x >= n1 - R);
+        stcol[c] = (lc >= TR) && (lc < TR + VW) && (x < n1);
+      }
+
+      double win[T][W][C];
+#pragma unroll
+      for (int s = 0; s < T; ++s)
+#pragma unroll
+        for (int w = 0; w < W; ++w)
+#pragma unroll
+          for (int c = 0; c < C; ++c) win[s][w][c] = 0.0;
+
+      for (int kbase = ka; kbase < kend; kbase += W) {
+#pragma unroll
+        for (int uu = 0; uu < W; ++uu) {
+          const int k = kbase + uu;
+          // ---- level 0: next input row from the TMA ring -------------------
+          // (the select keeps the window write unconditional, so the dead
+          // oldest row never stays live across the advance)
+          {
+            double v[C];
+            if (k < kb) {
+              const uint32_t pos = ring_cnt + (uint32_t)(k - ka);
+              const uint32_t slot = pos & (S - 1);
+              mbar_wait(&bars[slot], (pos / S) & 1);
+              const double* rowp = ring + slot * Cfg::LC + lane * C;
+              if constexpr (C % 2 == 0) {
+#pragma unroll
+                for (int c = 0; c < C; c += 2) {
+                  const double2 t2 = *reinterpret_cast<const double2*>(rowp + c);
+                  v[c] = t2.x;
+                  v[c + 1] = t2.y;
+                }
+              } else {
+#pragma unroll
+                for (int c = 0; c < C; ++c) v[c] = rowp[c];
+              }
+              __syncwarp();
+              if (lane == 0 && k + S < kb) {
+                fence_proxy_async_shared();
+                mbar_arrive_expect_tx(&bars[slot], Cfg::ROW_BYTES);
+                tma_load_2d(ring + slot * Cfg::LC, tm, X0, k + S, &bars[slot]);
+              }
+            } else {
+#pragma unroll
+              for (int c = 0; c < C; ++c) v[c] = 0.0;
+            }
+#pragma unroll
+            for (int c = 0; c < C; ++c) win[0][uu][c] = v[c];
+          }
+          // ---- levels 1..T ---------------------------------------------------
+          // Every level runs every advance.  During pipeline warm-up a level's
+          // target row is not yet valid (it depends on rows before ka) and it
+          // computes harmless values that no valid row ever consumes: level s
+          // row q is valid iff q >= ka + s*R (or the segment starts at the
+          // top frame), and level s+1 only reads rows >= q' - R of it.
+          static_for<T>([&](auto sI) {
+            constexpr int s = decltype(sI)::value + 1;  // level being produced
+            const int q = k - s * R;                    // its target row
+            double nv[C];
+            if (q < R || q >= n0 - R) {
+              // frame row (or warm-up row outside the grid): value carries over
+#pragma unroll
+              for (int c = 0; c < C; ++c) nv[c] = win[s - 1][pmod<W>(uu - s * R)][c];
+            } else {
+              // horizontal halos (only rows whose taps leave the lane's columns)
+              double hl[W][R], hr[W][R];
+              static_for<W>([&](auto wI) {
+                constexpr int dy = decltype(wI)::value - R;
+                if constexpr (row_has_halo<SH>(dy)) {
+                  constexpr int sl_off = dy;
+                  static_for<R>([&](auto jI) {
+                    constexpr int j = decltype(jI)::value;
+                    constexpr int ccl = -R + j;
+                    constexpr int dl = (-ccl + C - 1) / C;
+                    constexpr int coll = ccl + dl * C;
+                    constexpr int ccr = C + j;
+                    constexpr int dr = ccr / C;
+                    constexpr int colr = ccr - dr * C;
+                    const int sl = pmod<W>(uu - s * R + sl_off);
+                    hl[wI][j] = __shfl_up_sync(kFullMask, win[s - 1][sl][coll], dl);
+                    hr[wI][j] = __shfl_down_sync(kFullMask, win[s - 1][sl][colr], dr);
+                  });
+                }
+              });
+#pragma unroll
+              for (int c = 0; c < C; ++c) {
+                double acc = 0.0;
+                static_for<SH::NT>([&](auto iI) {
+                  constexpr int i = decltype(iI)::value;
+                  constexpr Off o = SH::tap(i);
+                  const int sl = pmod<W>(uu - s * R + o.d0);
+                  const int cc = c + o.d1;
+                  double x;
+                  if (cc < 0)
+                    x = hl[o.d0 + R][cc + R];
+                  else if (cc >= C)
+                    x = hr[o.d0 + R][cc - C];
+                  else
+                    x = win[s - 1][sl][cc];
+                  if constexpr (i == 0)
+                    acc = tap_first<EXACT>(cf.c[0], x);
+                  else
+                    acc = tap_next<EXACT>(acc, cf.c[i], x);
+                });
+                nv[c] = fcol[c] ? win[s - 1][pmod<W>(uu - s * R)][c] : acc;
+              }
+            }
+            if constexpr (s < T) {
+#pragma unroll
+              for (int c = 0; c < C; ++c) win[s][pmod<W>(uu - s * R)][c] = nv[c];
+            } else {
+              if (q >= r0 && q < r1) {
+                double* orow = out + (size_t)q * (size_t)n1 + (X0 + lane * C);
+#pragma unroll
+                for (int c = 0; c < C; ++c)
+                  if (stcol[c]) orow[c] = nv[c];
+              }
+            }
+          });
+        }
+      }
+      ring_cnt += (uint32_t)(kb - ka);
+    }
+
+    if (e + 1 < a.epochs) {
+      // Make this epoch's generic-proxy stores visible to the next epoch's
+      // TMA (async-proxy) loads issued by other CTAs.
+      fence_proxy_async_global();
+      __threadfence();
+      cooperative_groups::this_grid().sync();
+      fence_proxy_async_global();
+    }
+    const int nsrc = dst;
+    dst = (dst == BUF_OUT) ? BUF_SCR : BUF_OUT;
+    src = nsrc;
+  }
+}
+
+}  // namespace ebisu

@@ -1,0 +1,57 @@
+// ebisu_tb_launch.cuh -- host launch wrappers + registry entries for the
+// temporal-blocking kernel instantiations.
+#pragma once
+
+#include <string.h>
+
+#include "ebisu_internal.h"
+#include "ebisu_stream2d.cuh"
+
+namespace ebisu {
+
+template <class SH, int T, int C, int NW, int S, bool EXACT, int MINB>
+cudaError_t launch_stream2d(const TbLaunch& L) {
+  using Cfg = Stream2DCfg<SH, T, C, NW, S>;
+  auto kern = k_stream2d<SH, T, C, NW, S, EXACT, MINB>;
+  cudaError_t err =
+      cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg::SMEM_BYTES);
+  if (err != cudaSuccess) return err;
+  TmapSet maps;
+  memcpy(&maps.m[0], L.maps, 3 * sizeof(CUtensorMap));
+  Stream2DArgs a;
+  a.n0 = L.n0;
+  a.n1 = L.n1;
+  a.nstrips = L.nstrips;
+  a.nseg = L.nseg;
+  a.seg_len = L.seg_len;
+  a.epochs = L.epochs;
+  a.first_src = L.first_src;
+  a.first_dst = L.first_dst;
+  for (int i = 0; i < 3; ++i) a.buf[i] = L.buf[i];
+  Coefs<SH::NT> cf;
+  for (int i = 0; i < SH::NT; ++i) cf.c[i] = L.coeffs[i];
+  if (L.cooperative) {
+    void* args[] = {(void*)&maps, (void*)&a, (void*)&cf};
+    return cudaLaunchCooperativeKernel((const void*)kern, dim3(L.grid), dim3(NW * 32), args,
+                                       (size_t)Cfg::SMEM_BYTES, L.stream);
+  }
+  kern<<<L.grid, NW * 32, Cfg::SMEM_BYTES, L.stream>>>(maps, a, cf);
+  return cudaGetLastError();
+}
+
+// Register-budget heuristic: the window holds ~T*2R*C doubles live.
+constexpr int s2d_minb(int T, int R, int C, int NW) {
+  const int est = 4 * T * R * C + 48;
+  int m = 65536 / (NW * 32 * (est < 64 ? 64 : est));
+  return m < 1 ? 1 : (m > 8 ? 8 : m);
+}
+
+#define EBISU_S2D_ENTRY(SHAPE_ID, SH, T, C, NW, S, EX)                                         \
+  TbKernel {                                                                                  \
+    SHAPE_ID, 2, T, C, NW, S, EX, Stream2DCfg<SH, T, C, NW, S>::SMEM_BYTES, 32 * C, 1, 1,      \
+        Stream2DCfg<SH, T, C, NW, S>::VW, 0,                                                  \
+        (const void*)&k_stream2d<SH, T, C, NW, S, (EX) != 0, s2d_minb(T, SH::R, C, NW)>,      \
+        &launch_stream2d<SH, T, C, NW, S, (EX) != 0, s2d_minb(T, SH::R, C, NW)>               \
+  }
+
+}  // namespace ebisu

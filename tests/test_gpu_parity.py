@@ -1,0 +1,205 @@
+"""GPU parity: the sm_100a path through the C ABI vs the oracle / golden
+fixtures.  Bar: bitwise in exact mode (IEEE binary64 mul/add in tap order),
+1e-12 relative (of max |ref|) in FMA mode.  (north_star tolerance: 1e-12 fp64.)
+"""
+
+from __future__ import annotations
+
+import os
+
+import numpy as np
+import pytest
+
+import paper_2305_07390_b200 as eb
+from conftest import sha256, taps_of
+from oracle import reference_run as oracle_run
+from oracle import reference_run_threaded
+from paper_2305_07390_b200 import _native
+
+pytestmark = pytest.mark.gpu
+
+FMA_RTOL = 1e-12
+
+
+def _shape(name):
+    return eb.get_shape(name)
+
+
+def test_library_is_the_native_one():
+    lib = _native.load()
+    assert lib.ebisu_device_count() >= 1
+    assert os.path.samefile(lib._name, _native.LIB_PATH)
+
+
+def test_golden_cases_bitwise_auto(golden):
+    for rec in golden["cases"]:
+        st = _shape(rec["name"])
+        g = eb.random_grid(rec["extents"], rec["seed"])
+        out, tr = eb.sweep(g, st, rec["steps"], trace=True)
+        assert sha256(out.cells) == rec["output_sha256"], (rec["id"], rec["name"], tr)
+
+
+@pytest.mark.parametrize("t", list(range(1, 17)))
+def test_j2d5pt_every_depth_bitwise(golden, t):
+    # BASELINE config 1 (512^2, 100 steps) and a ragged 200x260 case, every fused depth
+    for rec in golden["cases"]:
+        if rec["name"] != "j2d5pt" or rec["extents"] not in ([512, 512], [200, 260],
+                                                             [96, 1024]):
+            continue
+        g = eb.random_grid(rec["extents"], rec["seed"])
+        for persistent in (True, False):
+            out, tr = eb.sweep(g, _shape("j2d5pt"), rec["steps"], t=t, persistent=persistent,
+                               trace=True)
+            assert tr["kernel"] == "stream2d_tb", tr
+            assert sha256(out.cells) == rec["output_sha256"], (rec["id"], t, persistent)
+
+
+CASES_2D = {
+    "j2d5pt": list(range(1, 17)),
+    "j2d9pt-gol": [1, 2, 3, 4, 6, 8],
+    "j2d9pt": [1, 2, 3, 4, 5],
+    "j2d25pt": [1, 2, 3, 4],
+    "j2d13pt": [1, 2, 3],
+    "j2ds25pt": [1, 2],
+}
+
+
+@pytest.mark.parametrize("name", list(CASES_2D))
+def test_2d_shapes_all_depths_ragged(name):
+    st = _shape(name)
+    rng = eb.SplitMix64(hash(name) & 0xFFFF)
+    for t in CASES_2D[name]:
+        for _ in range(3):
+            n0 = 2 * st.radius + 1 + rng.randint(0, 300)
+            n1 = 2 * (st.radius + 1 + rng.randint(0, 400) // 2)  # even width -> TMA path
+            steps = rng.randint(1, 3 * t + 2)
+            g = eb.random_grid((n0, n1), rng.next_u64())
+            ref = oracle_run(g.cells, taps_of(st), steps)
+            out, tr = eb.sweep(g, st, steps, t=t, trace=True)
+            assert np.array_equal(out.cells, ref), (name, t, (n0, n1), steps, tr)
+
+
+def test_odd_width_and_generic_shapes_use_naive_kernel():
+    # odd row pitch (TMA needs 16-byte strides) and non-catalog tap orders
+    st = _shape("j2d5pt")
+    g = eb.random_grid((37, 131), 5)
+    out, tr = eb.sweep(g, st, 23, trace=True)
+    assert np.array_equal(out.cells, oracle_run(g.cells, taps_of(st), 23))
+    # reversed tap order = a different summation order -> generic kernel, still exact
+    rev = eb.StencilShape("rev", 2, tuple(reversed(st.taps)), 10, 2, 6, 4.0)
+    g = eb.random_grid((40, 64), 9)
+    out, tr = eb.sweep(g, rev, 7, trace=True)
+    assert tr["kernel"] == "naive_step"
+    assert np.array_equal(out.cells, oracle_run(g.cells, taps_of(rev), 7))
+
+
+@pytest.mark.parametrize("name", ["j1d3pt", "j3d7pt", "j3d13pt", "j3d17pt", "j3d27pt",
+                                  "poisson"])
+def test_other_dims_bitwise(name):
+    st = _shape(name)
+    ext = {1: (301,), 3: (17, 19, 24)}[st.dims]
+    g = eb.random_grid(ext, 77)
+    out = eb.reference_run(g, st, 6)
+    assert np.array_equal(out.cells, oracle_run(g.cells, taps_of(st), 6))
+
+
+@pytest.mark.parametrize("name", ["j2d5pt", "j2d25pt", "j3d7pt"])
+def test_fma_mode_within_tolerance(name):
+    st = _shape(name)
+    ext = (130, 258) if st.dims == 2 else (20, 30, 34)
+    g = eb.random_grid(ext, 4)
+    out = eb.sweep(g, st, 20, exact=False)
+    ref = oracle_run(g.cells, taps_of(st), 20)
+    err = np.max(np.abs(out.cells - ref))
+    assert err <= FMA_RTOL * np.max(np.abs(ref)), err
+
+
+def test_coefficients_are_runtime():
+    st = eb.make_benchmark("j2d5pt", coefficients=[0.1, 0.3, 0.2, 0.25, 0.15])
+    g = eb.random_grid((64, 128), 3)
+    assert np.array_equal(eb.reference_run(g, st, 9).cells,
+                          oracle_run(g.cells, taps_of(st), 9))
+
+
+def test_purity_and_boundary_tag():
+    st = eb.make_benchmark("j2d5pt")
+    g = eb.Grid(eb.random_grid((10, 10), seed=5).cells, "skip-update")
+    before = g.cells.copy()
+    out = eb.reference_run(g, st, 3)
+    assert np.array_equal(g.cells, before)
+    assert out.boundary == "skip-update"
+
+
+def test_engines_reference_style(rng):
+    # reference tests/conftest.py:21-100 case generators, engine vs oracle
+    for name in ("j2d5pt", "j2d9pt", "j2d9pt-gol", "j2d25pt", "j1d3pt", "j3d7pt", "j3d27pt"):
+        st = eb.make_benchmark(name)
+        rad = st.radius
+        for _ in range(5):
+            t = rng.randint(1, 3)
+            core = rng.randint(max(4, rad * 2), 10)
+            tile = core + 2 * rad * t
+            if st.dims == 1:
+                params = eb.TilingParams(scheme=eb.SM_TILING, t=t, tile=(tile,))
+                domain = (rng.randint(1, 3) * core + 2 * rad,)
+            elif st.dims == 2:
+                params = eb.TilingParams(scheme=eb.SM_TILING, t=t, tile=(tile,))
+                domain = (2 * rad + rng.randint(6, 14), rng.randint(1, 3) * core + 2 * rad)
+            else:
+                params = eb.TilingParams(scheme=eb.SM_TILING, t=t, tile=(tile, tile))
+                domain = (2 * rad + rng.randint(6, 14), rng.randint(1, 2) * core + 2 * rad,
+                          rng.randint(1, 2) * core + 2 * rad)
+            g = eb.random_grid(domain, rng.next_u64())
+            out, trace = eb.run_sm_tiling(g, st, params)
+            assert np.array_equal(out.cells, oracle_run(g.cells, taps_of(st), t)), (name, domain)
+            assert trace.cells_valid > 0
+            s = eb.trace_summary(trace, st, params, domain)
+            assert s.a_gm_measured > 0
+
+
+# ---- device-resident path at BASELINE sizes -------------------------------------
+
+
+def _torch():
+    import torch
+
+    return torch
+
+
+def test_device_rng_bit_identical():
+    from paper_2305_07390_b200 import device
+
+    d = device.random_grid_device((257, 129), seed=99)
+    assert np.array_equal(d.cpu().numpy(), eb.random_grid((257, 129), 99).cells)
+
+
+def test_full_size_8192_against_oracle():
+    # BASELINE config 2 geometry: t=8 epoch + remainder through the 1-step kernel.
+    from paper_2305_07390_b200 import device
+
+    torch = _torch()
+    st = eb.make_benchmark("j2d5pt")
+    steps = 9
+    d_in = device.random_grid_device((8192, 8192), seed=1)
+    out = device.sweep_device(d_in, st, steps, t=8)
+    torch.cuda.synchronize()
+    ref = reference_run_threaded(d_in.cpu().numpy(), taps_of(st), steps, os.cpu_count() or 4)
+    assert np.array_equal(out.cpu().numpy(), ref)
+
+
+def test_full_size_composition_and_persistence():
+    # size-independent properties at full size: run(16) == run(8) o run(8), and
+    # persistent (cooperative, grid.sync) == one launch per epoch, bitwise.
+    from paper_2305_07390_b200 import device
+
+    torch = _torch()
+    st = eb.make_benchmark("j2d5pt")
+    d_in = device.random_grid_device((8192, 8192), seed=2)
+    a = device.sweep_device(d_in, st, 48, t=8, persistent=True)
+    b = device.sweep_device(d_in, st, 48, t=8, persistent=False)
+    h = device.sweep_device(device.sweep_device(d_in, st, 24, t=8), st, 24, t=6)
+    torch.cuda.synchronize()
+    assert device.compare_device(a, b)["mismatches"] == 0
+    assert device.compare_device(a, h)["mismatches"] == 0
+    # maximum principle (convex coefficients): values stay in [min, max] of input
+    assert float(a.max()) <= float(d_in.max()) and float(a.min()) >= float(d_in.min())
