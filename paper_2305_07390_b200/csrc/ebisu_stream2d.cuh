@@ -55,7 +55,10 @@ struct Stream2DCfg {
   static constexpr int R = SH::R;
   static constexpr int W = 2 * R + 1;       // window rows per level
   static constexpr int LC = 32 * C;         // loaded columns per warp
-  static constexpr int VW = LC - 2 * T * R; // valid columns per warp
+  // Column halo rounded up to even: a TMA box must start on a 16-byte
+  // boundary in the innermost dimension (2 doubles).
+  static constexpr int HX = (T * R + 1) & ~1;
+  static constexpr int VW = LC - 2 * HX;    // valid columns per warp (even)
   static constexpr int ROW_BYTES = LC * 8;
   static constexpr int RING_BYTES = S * ROW_BYTES;
   static constexpr int SMEM_BYTES = NW * RING_BYTES + NW * S * 8;
@@ -86,6 +89,7 @@ __global__ void __launch_bounds__(NW * 32, MINB)
   constexpr int W = Cfg::W;
   constexpr int VW = Cfg::VW;
   constexpr int TR = T * R;
+  constexpr int HX = Cfg::HX;
 
   extern __shared__ __align__(1024) unsigned char smem[];
   const int warp = threadIdx.x >> 5;
@@ -117,7 +121,7 @@ __global__ void __launch_bounds__(NW * 32, MINB)
     for (int u = gwarp; u < units; u += nwarps) {
       const int strip = u % a.nstrips;
       const int seg = u / a.nstrips;
-      const int X0 = strip * VW - TR;  // global column of loaded column 0
+      const int X0 = strip * VW - HX;  // global column of loaded column 0 (even)
       const int r0 = seg * a.seg_len;
       const int r1 = min(n0, r0 + a.seg_len);
       const int ka = max(0, r0 - TR);
@@ -141,7 +145,7 @@ __global__ void __launch_bounds__(NW * 32, MINB)
         const int lc = lane * C + c;
         const int x = X0 + lc;
         fcol[c] = (x < R) || (x >= n1 - R);
-        stcol[c] = (lc >= TR) && (lc < TR + VW) && (x < n1);
+        stcol[c] = (lc >= HX) && (lc < HX + VW) && (x < n1);
       }
 
       double win[T][W][C];
