@@ -89,7 +89,9 @@ typedef struct ebisu_params {
   int32_t exact;             /* 1: bitwise (no FMA contraction); 0: FMA chain      */
   int32_t persistent;        /* 1: one cooperative launch, grid sync between epochs */
   int32_t validate_tile;     /* 1: apply the reference TilingParams.validate rules  */
-  int32_t reserved[6];
+  int32_t lane_cells;        /* cells per lane along the fastest axis (0 = planner) */
+  int32_t seg_rows;          /* rows per work unit along axis 0 (0 = planner)       */
+  int32_t reserved[4];
 } ebisu_params;
 
 /* Closed-form execution counters of the GPU run (reference ExecutionTrace,

@@ -14,7 +14,8 @@ import threading
 import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libebisu.so")
+# EBISU_LIB_PATH lets experiments A/B alternative builds of the same ABI.
+LIB_PATH = os.environ.get("EBISU_LIB_PATH") or os.path.join(_HERE, "libebisu.so")
 
 EBISU_OK = 0
 EBISU_ERR_VALUE = 1
@@ -70,7 +71,9 @@ class ParamsC(ctypes.Structure):
         ("exact", ctypes.c_int32),
         ("persistent", ctypes.c_int32),
         ("validate_tile", ctypes.c_int32),
-        ("reserved", ctypes.c_int32 * 6),
+        ("lane_cells", ctypes.c_int32),
+        ("seg_rows", ctypes.c_int32),
+        ("reserved", ctypes.c_int32 * 4),
     ]
 
 
@@ -186,7 +189,8 @@ class StencilArgs:
 
 def make_params(scheme: int = SCHEME_AUTO, t: int = 0, tile=(0, 0), device_tile_grid=(0, 0),
                 lazy: bool = False, exact: bool = True, persistent: bool = True,
-                validate_tile: bool = False) -> ParamsC:
+                validate_tile: bool = False, lane_cells: int = 0,
+                seg_rows: int = 0) -> ParamsC:
     p = ParamsC()
     p.scheme = scheme
     p.t = int(t)
@@ -198,6 +202,8 @@ def make_params(scheme: int = SCHEME_AUTO, t: int = 0, tile=(0, 0), device_tile_
     p.exact = int(bool(exact))
     p.persistent = int(bool(persistent))
     p.validate_tile = int(bool(validate_tile))
+    p.lane_cells = int(lane_cells)
+    p.seg_rows = int(seg_rows)
     return p
 
 

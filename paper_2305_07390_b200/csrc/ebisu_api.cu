@@ -236,12 +236,14 @@ enum KernelId : int {
   KID_STREAM3D = 3,
 };
 
-const TbKernel* find_tb(int shape_id, int dims, int T, bool exact) {
+// First registered kernel for (shape, depth, exactness) -- the registry lists
+// the planner's default lane width first -- or the one with lane width C.
+const TbKernel* find_tb(int shape_id, int dims, int T, bool exact, int C = 0) {
   int n = 0;
   const TbKernel* ks = tb_kernels(&n);
   for (int i = 0; i < n; ++i)
     if (ks[i].shape_id == shape_id && ks[i].dims == dims && ks[i].T == T &&
-        (ks[i].exact != 0) == exact)
+        (ks[i].exact != 0) == exact && (C == 0 || ks[i].C == C))
       return &ks[i];
   return nullptr;
 }
@@ -260,7 +262,7 @@ int best_depth_leq(int shape_id, int dims, int tmax, bool exact) {
 // Default fused depth (measured sweet spot on B200).
 int default_depth(int shape_id) {
   switch (shape_id) {
-    case SHAPE_J2D5PT: return 8;
+    case SHAPE_J2D5PT: return 4;
     case SHAPE_J2D9PT_GOL: return 6;
     case SHAPE_J2D9PT: return 4;
     case SHAPE_J2D25PT: return 3;
@@ -284,7 +286,7 @@ struct Counters {
 
 int run_tb2d_stage(const ProblemDesc& p, const TbKernel* k, int epochs, int first_src,
                    int first_dst, double* bufs[3], const CUtensorMap maps[3], bool coop_req,
-                   const DevInfo& di, cudaStream_t st, Counters* ctr) {
+                   int seg_rows_req, const DevInfo& di, cudaStream_t st, Counters* ctr) {
   const int n0 = (int)p.ext[0], n1 = (int)p.ext[1];
   const int T = k->T, R = p.rad;
   int per_sm = 0;
@@ -303,6 +305,7 @@ int run_tb2d_stage(const ProblemDesc& p, const TbKernel* k, int epochs, int firs
   const int min_len = std::max(32, 4 * T * R);
   int seg_len = (n0 + nseg - 1) / nseg;
   if (seg_len < min_len) seg_len = min_len;
+  if (seg_rows_req > 0) seg_len = seg_rows_req;
   nseg = (n0 + seg_len - 1) / seg_len;
   const long long units = (long long)nstrips * nseg;
   int grid = (int)std::min<long long>(max_ctas, (units + k->NW - 1) / k->NW);
@@ -383,7 +386,9 @@ int run_device_impl(const ProblemDesc& p, const double* d_in, double* d_out, dou
                (reinterpret_cast<uintptr_t>(d_out) % 16 == 0);
   if (tb_ok) {
     int t = (prm && prm->t > 0) ? prm->t : default_depth(p.shape_id);
-    const TbKernel* k = find_tb(p.shape_id, 2, t, exact);
+    const int want_c = prm ? prm->lane_cells : 0;
+    const TbKernel* k = find_tb(p.shape_id, 2, t, exact, want_c);
+    if (!k && want_c) return fail(EBISU_ERR_UNSUPPORTED, "no kernel with depth %d and %d cells per lane", t, want_c);
     if (!k) {
       // depth not instantiated: compose the sweep from the deepest kernel
       // below it (epochs compose bitwise, test_grid.py:94-117)
@@ -464,7 +469,8 @@ int run_device_impl(const ProblemDesc& p, const double* d_in, double* d_out, dou
         }
         if (result) break;
       }
-      result = run_tb2d_stage(p, s.k, s.epochs, src, dst, bufs, maps, coop, di, st, ctr);
+      result = run_tb2d_stage(p, s.k, s.epochs, src, dst, bufs, maps, coop,
+                              prm ? prm->seg_rows : 0, di, st, ctr);
       if (result) break;
       src = (s.epochs % 2 == 1) ? dst : (dst == BUF_OUT ? BUF_SCR : BUF_OUT);
     }

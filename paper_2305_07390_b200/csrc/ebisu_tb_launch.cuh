@@ -40,9 +40,12 @@ cudaError_t launch_stream2d(const TbLaunch& L) {
 }
 
 // Register-budget heuristic: the window holds ~T*2R*C doubles live.
+#ifndef EBISU_MINB_BIAS
+#define EBISU_MINB_BIAS 0
+#endif
 constexpr int s2d_minb(int T, int R, int C, int NW) {
   const int est = 4 * T * R * C + 48;
-  int m = 65536 / (NW * 32 * (est < 64 ? 64 : est));
+  int m = 65536 / (NW * 32 * (est < 64 ? 64 : est)) + EBISU_MINB_BIAS;
   return m < 1 ? 1 : (m > 8 ? 8 : m);
 }
 
