@@ -39,7 +39,7 @@ sys.path.insert(0, ROOT)
 N0 = N1 = 8192
 TSTEPS = 1000
 STENCIL = "j2d5pt"
-DEPTH = 4
+DEPTH = 8
 ALG_BYTES_PER_CELL_STEP = 16  # 8 B load + 8 B store of the naive sweep
 
 

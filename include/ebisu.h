@@ -91,7 +91,8 @@ typedef struct ebisu_params {
   int32_t validate_tile;     /* 1: apply the reference TilingParams.validate rules  */
   int32_t lane_cells;        /* cells per lane along the fastest axis (0 = planner) */
   int32_t seg_rows;          /* rows per work unit along axis 0 (0 = planner)       */
-  int32_t reserved[4];
+  int32_t variant;           /* n-th registered kernel for (shape, t) (0 = default) */
+  int32_t reserved[3];
 } ebisu_params;
 
 /* Closed-form execution counters of the GPU run (reference ExecutionTrace,

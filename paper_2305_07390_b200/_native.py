@@ -73,7 +73,8 @@ class ParamsC(ctypes.Structure):
         ("validate_tile", ctypes.c_int32),
         ("lane_cells", ctypes.c_int32),
         ("seg_rows", ctypes.c_int32),
-        ("reserved", ctypes.c_int32 * 4),
+        ("variant", ctypes.c_int32),
+        ("reserved", ctypes.c_int32 * 3),
     ]
 
 
@@ -190,7 +191,7 @@ class StencilArgs:
 def make_params(scheme: int = SCHEME_AUTO, t: int = 0, tile=(0, 0), device_tile_grid=(0, 0),
                 lazy: bool = False, exact: bool = True, persistent: bool = True,
                 validate_tile: bool = False, lane_cells: int = 0,
-                seg_rows: int = 0) -> ParamsC:
+                seg_rows: int = 0, variant: int = 0) -> ParamsC:
     p = ParamsC()
     p.scheme = scheme
     p.t = int(t)
@@ -204,6 +205,7 @@ def make_params(scheme: int = SCHEME_AUTO, t: int = 0, tile=(0, 0), device_tile_
     p.validate_tile = int(bool(validate_tile))
     p.lane_cells = int(lane_cells)
     p.seg_rows = int(seg_rows)
+    p.variant = int(variant)
     return p
 
 

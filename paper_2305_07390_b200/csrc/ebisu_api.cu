@@ -10,6 +10,7 @@
 #include <cudaTypedefs.h>
 #include <stdarg.h>
 #include <stdio.h>
+#include <stdlib.h>
 
 #include <algorithm>
 #include <mutex>
@@ -19,6 +20,7 @@
 #include "ebisu_internal.h"
 #include "ebisu_common.cuh"
 #include "ebisu_shapes.cuh"
+#include "ebisu_stream2d.cuh"
 
 namespace ebisu {
 namespace {
@@ -238,13 +240,14 @@ enum KernelId : int {
 
 // First registered kernel for (shape, depth, exactness) -- the registry lists
 // the planner's default lane width first -- or the one with lane width C.
-const TbKernel* find_tb(int shape_id, int dims, int T, bool exact, int C = 0) {
+const TbKernel* find_tb(int shape_id, int dims, int T, bool exact, int C = 0, int variant = 0) {
   int n = 0;
   const TbKernel* ks = tb_kernels(&n);
   for (int i = 0; i < n; ++i)
     if (ks[i].shape_id == shape_id && ks[i].dims == dims && ks[i].T == T &&
-        (ks[i].exact != 0) == exact && (C == 0 || ks[i].C == C))
-      return &ks[i];
+        (ks[i].exact != 0) == exact && (C == 0 || ks[i].C == C)) {
+      if (variant-- == 0) return &ks[i];
+    }
   return nullptr;
 }
 
@@ -262,12 +265,17 @@ int best_depth_leq(int shape_id, int dims, int tmax, bool exact) {
 // Default fused depth (measured sweet spot on B200).
 int default_depth(int shape_id) {
   switch (shape_id) {
-    case SHAPE_J2D5PT: return 4;
+    case SHAPE_J2D5PT: return 8;
     case SHAPE_J2D9PT_GOL: return 6;
     case SHAPE_J2D9PT: return 4;
     case SHAPE_J2D25PT: return 3;
     case SHAPE_J2D13PT: return 2;
     case SHAPE_J2DS25PT: return 2;
+    case SHAPE_J3D7PT: return 2;
+    case SHAPE_J3D13PT: return 2;
+    case SHAPE_J3D27PT: return 2;
+    case SHAPE_J3D17PT: return 2;
+    case SHAPE_POISSON: return 2;
     default: return 4;
   }
 }
@@ -280,9 +288,40 @@ struct Stage {
 
 struct Counters {
   uint64_t gm_loads = 0, gm_stores = 0, cells_computed = 0, device_tiles = 0, syncs_device = 0,
-           launches = 0;
+           syncs_block = 0, launches = 0;
   int grid = 0, nw = 0, t_used = 0, kid = KID_NONE;
 };
+
+// Row (axis-0) segmentation of the work units.  Every unit pays a pipeline
+// warm-up of `warm` advances; units are handed out dynamically to `slots`
+// concurrent workers, so an epoch takes about units*(len+warm)/slots plus a
+// tail of up to one unit.  Minimise that estimate.
+void plan_segments(int n0, long long tiles, long long slots, int warm, int min_len,
+                   int* nseg_out, int* seg_len_out) {
+  double best = 1e300;
+  int best_len = n0;
+  for (int nseg = 1; nseg <= 4096 && nseg <= n0; ++nseg) {
+    const int len = (n0 + nseg - 1) / nseg;
+    if (len < min_len && nseg > 1) break;
+    const int ns = (n0 + len - 1) / len;
+    const double units = (double)tiles * ns;
+    const double unit_cost = (double)(len + warm);
+    const double cost = std::max(units / (double)slots, 1.0) * unit_cost + 0.5 * unit_cost;
+    if (cost < best * 0.999) {
+      best = cost;
+      best_len = len;
+    }
+  }
+  *seg_len_out = best_len;
+  *nseg_out = (n0 + best_len - 1) / best_len;
+}
+
+// Per-epoch dynamic-scheduling counters for one stage (zeroed on `st`).
+int alloc_work(int epochs, cudaStream_t st, int** out) {
+  EB_CUDA(cudaMallocAsync((void**)out, sizeof(int) * (size_t)std::max(epochs, 1), st));
+  EB_CUDA(cudaMemsetAsync(*out, 0, sizeof(int) * (size_t)std::max(epochs, 1), st));
+  return EBISU_OK;
+}
 
 int run_tb2d_stage(const ProblemDesc& p, const TbKernel* k, int epochs, int first_src,
                    int first_dst, double* bufs[3], const CUtensorMap maps[3], bool coop_req,
@@ -298,16 +337,17 @@ int run_tb2d_stage(const ProblemDesc& p, const TbKernel* k, int epochs, int firs
   const int max_ctas = per_sm * di.sms;
   const int total_warps = max_ctas * k->NW;
   const int VW = k->valid_x;
-  const int nstrips = (n1 + VW - 1) / VW;
-  // Row segments: one unit per resident warp, but never shorter than the
-  // pipeline warm-up (2*T*R rows) so redundant work stays small.
-  int nseg = std::max(1, total_warps / nstrips);
-  const int min_len = std::max(32, 4 * T * R);
-  int seg_len = (n0 + nseg - 1) / nseg;
-  if (seg_len < min_len) seg_len = min_len;
-  if (seg_rows_req > 0) seg_len = seg_rows_req;
-  nseg = (n0 + seg_len - 1) / seg_len;
+  const int LC = k->box0, HX = (LC - VW) / 2;
+  int aligned = 0;
+  const int nstrips = stream2d_nstrips(n1, LC, VW, HX, R, k->C, &aligned);
+  int nseg = 1, seg_len = n0;
+  plan_segments(n0, nstrips, total_warps, 2 * T * R, std::max(16, 2 * T * R), &nseg, &seg_len);
+  if (seg_rows_req > 0) {
+    seg_len = seg_rows_req;
+    nseg = (n0 + seg_len - 1) / seg_len;
+  }
   const long long units = (long long)nstrips * nseg;
+  // every resident warp pulls units dynamically
   int grid = (int)std::min<long long>(max_ctas, (units + k->NW - 1) / k->NW);
   if (grid < 1) grid = 1;
   const bool coop = coop_req && di.coop && epochs > 1;
@@ -320,14 +360,25 @@ int run_tb2d_stage(const ProblemDesc& p, const TbKernel* k, int epochs, int firs
   L.seg_len = seg_len;
   L.first_src = first_src;
   L.first_dst = first_dst;
+  L.aligned = aligned;
   for (int i = 0; i < 3; ++i) L.buf[i] = bufs[i];
   L.maps = maps;
   L.coeffs = p.coeffs;
   L.grid = grid;
   L.stream = st;
+  long long* clk = nullptr;
+  const char* clk_path = getenv("EBISU_UNIT_CLOCK");
+  if (clk_path && *clk_path) {
+    EB_CUDA(cudaMallocAsync((void**)&clk, sizeof(long long) * 2 * units, st));
+    EB_CUDA(cudaMemsetAsync(clk, 0, sizeof(long long) * 2 * units, st));
+    L.unit_clock = clk;
+  }
+  int* work = nullptr;
+  if (int rc = alloc_work(epochs, st, &work)) return rc;
   if (coop) {
     L.epochs = epochs;
     L.cooperative = true;
+    L.work = work;
     EB_CUDA(k->launch(L));
     ctr->launches += 1;
     ctr->syncs_device += (uint64_t)(epochs - 1);
@@ -338,10 +389,26 @@ int run_tb2d_stage(const ProblemDesc& p, const TbKernel* k, int epochs, int firs
       L.first_src = src;
       L.first_dst = dst;
       L.cooperative = false;
+      L.work = work + e;
       EB_CUDA(k->launch(L));
       ctr->launches += 1;
       src = dst;
       dst = (dst == BUF_OUT) ? BUF_SCR : BUF_OUT;
+    }
+  }
+  cudaFreeAsync(work, st);
+  if (clk) {
+    std::vector<long long> h(2 * units);
+    EB_CUDA(cudaMemcpyAsync(h.data(), clk, sizeof(long long) * 2 * units,
+                            cudaMemcpyDeviceToHost, st));
+    EB_CUDA(cudaStreamSynchronize(st));
+    cudaFreeAsync(clk, st);
+    if (FILE* f = fopen(clk_path, "w")) {
+      fprintf(f, "unit,strip,seg,start_ns,end_ns\n");
+      for (long long u = 0; u < units; ++u)
+        fprintf(f, "%lld,%lld,%lld,%lld,%lld\n", u, u % nstrips, u / nstrips, h[2 * u],
+                h[2 * u + 1]);
+      fclose(f);
     }
   }
   // closed-form counters (reference ExecutionTrace semantics, trace.py:1-17)
@@ -364,6 +431,90 @@ int run_tb2d_stage(const ProblemDesc& p, const TbKernel* k, int epochs, int firs
   return EBISU_OK;
 }
 
+int run_tb3d_stage(const ProblemDesc& p, const TbKernel* k, int epochs, int first_src,
+                   int first_dst, double* bufs[3], const CUtensorMap maps[3], bool coop_req,
+                   int seg_rows_req, const DevInfo& di, cudaStream_t st, Counters* ctr) {
+  const int n0 = (int)p.ext[0], n1 = (int)p.ext[1], n2 = (int)p.ext[2];
+  const int T = k->T, R = p.rad;
+  int per_sm = 0;
+  EB_CUDA(cudaFuncSetAttribute(k->func, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                               k->smem_bytes));
+  EB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k->func, k->NW * 32,
+                                                        (size_t)k->smem_bytes));
+  if (per_sm < 1) return fail(EBISU_ERR_CUDA, "stream3d kernel cannot be resident (T=%d)", T);
+  const int max_ctas = per_sm * di.sms;
+  const int ntx = (n2 + k->valid_x - 1) / k->valid_x;
+  const int nty = (n1 + k->valid_y - 1) / k->valid_y;
+  int nseg = 1, seg_len = n0;
+  plan_segments(n0, (long long)ntx * nty, max_ctas, 3 * T * R, std::max(8, 2 * T * R), &nseg,
+                &seg_len);
+  if (seg_rows_req > 0) {
+    seg_len = seg_rows_req;
+    nseg = (n0 + seg_len - 1) / seg_len;
+  }
+  const long long units = (long long)ntx * nty * nseg;
+  int grid = (int)std::min<long long>(max_ctas, units);
+  if (grid < 1) grid = 1;
+  const bool coop = coop_req && di.coop && epochs > 1;
+  TbLaunch L{};
+  L.n0 = n0;
+  L.n1 = n1;
+  L.n2 = n2;
+  L.ntx = ntx;
+  L.nty = nty;
+  L.nseg = nseg;
+  L.seg_len = seg_len;
+  for (int i = 0; i < 3; ++i) L.buf[i] = bufs[i];
+  L.maps = maps;
+  L.coeffs = p.coeffs;
+  L.grid = grid;
+  L.stream = st;
+  int* work = nullptr;
+  if (int rc = alloc_work(epochs, st, &work)) return rc;
+  if (coop) {
+    L.epochs = epochs;
+    L.first_src = first_src;
+    L.first_dst = first_dst;
+    L.cooperative = true;
+    L.work = work;
+    EB_CUDA(k->launch(L));
+    ctr->launches += 1;
+    ctr->syncs_device += (uint64_t)(epochs - 1);
+  } else {
+    int src = first_src, dst = first_dst;
+    for (int e = 0; e < epochs; ++e) {
+      L.epochs = 1;
+      L.first_src = src;
+      L.first_dst = dst;
+      L.cooperative = false;
+      L.work = work + e;
+      EB_CUDA(k->launch(L));
+      ctr->launches += 1;
+      src = dst;
+      dst = (dst == BUF_OUT) ? BUF_SCR : BUF_OUT;
+    }
+  }
+  cudaFreeAsync(work, st);
+  uint64_t loads = 0, adv = 0;
+  for (int g = 0; g < nseg; ++g) {
+    const int r0 = g * seg_len, r1 = std::min(n0, r0 + seg_len);
+    const int ka = std::max(0, r0 - T * R), kb = std::min(n0, r1 + T * R);
+    loads += (uint64_t)(kb - ka);
+    adv += (uint64_t)(r1 + T * R - ka);
+  }
+  const uint64_t tile_cells = (uint64_t)k->box0 * (uint64_t)k->box1;
+  ctr->gm_loads += (uint64_t)epochs * loads * tile_cells * (uint64_t)ntx * nty;
+  ctr->gm_stores += (uint64_t)epochs * (uint64_t)n0 * n1 * n2;
+  ctr->cells_computed += (uint64_t)epochs * adv * (uint64_t)T * tile_cells * (uint64_t)ntx * nty;
+  ctr->device_tiles += (uint64_t)epochs * (uint64_t)units;
+  ctr->syncs_block += (uint64_t)epochs * adv * (uint64_t)ntx * nty;
+  ctr->grid = grid;
+  ctr->nw = k->NW;
+  ctr->t_used = std::max(ctr->t_used, T);
+  ctr->kid = KID_STREAM3D;
+  return EBISU_OK;
+}
+
 int run_device_impl(const ProblemDesc& p, const double* d_in, double* d_out, double* d_scr,
                     long long steps, const ebisu_params* prm, cudaStream_t st, Counters* ctr) {
   DevInfo di;
@@ -381,34 +532,42 @@ int run_device_impl(const ProblemDesc& p, const double* d_in, double* d_out, dou
 
   // ---- plan the stage list ----------------------------------------------------
   std::vector<Stage> stages;
-  bool tb_ok = p.dims == 2 && p.shape_id != SHAPE_GENERIC && scheme != EBISU_SCHEME_NAIVE &&
-               (p.ext[1] % 2 == 0) && (reinterpret_cast<uintptr_t>(d_in) % 16 == 0) &&
-               (reinterpret_cast<uintptr_t>(d_out) % 16 == 0);
+  const int D = p.dims;
+  // TMA needs 16-byte row strides (even last extent) and 16-byte aligned bases.
+  bool tb_ok = (D == 2 || D == 3) && p.shape_id != SHAPE_GENERIC &&
+               scheme != EBISU_SCHEME_NAIVE && (p.ext[D - 1] % 2 == 0) &&
+               (reinterpret_cast<uintptr_t>(d_in) % 16 == 0) &&
+               (reinterpret_cast<uintptr_t>(d_out) % 16 == 0) &&
+               (!d_scr || reinterpret_cast<uintptr_t>(d_scr) % 16 == 0);
   if (tb_ok) {
     int t = (prm && prm->t > 0) ? prm->t : default_depth(p.shape_id);
     const int want_c = prm ? prm->lane_cells : 0;
-    const TbKernel* k = find_tb(p.shape_id, 2, t, exact, want_c);
-    if (!k && want_c) return fail(EBISU_ERR_UNSUPPORTED, "no kernel with depth %d and %d cells per lane", t, want_c);
+    const int want_v = prm ? prm->variant : 0;
+    const TbKernel* k = find_tb(p.shape_id, D, t, exact, want_c, want_v);
+    if (!k && (want_c || want_v))
+      return fail(EBISU_ERR_UNSUPPORTED, "no kernel with depth %d, %d cells per lane, variant %d",
+                  t, want_c, want_v);
     if (!k) {
       // depth not instantiated: compose the sweep from the deepest kernel
       // below it (epochs compose bitwise, test_grid.py:94-117)
-      t = best_depth_leq(p.shape_id, 2, t, exact);
-      k = t ? find_tb(p.shape_id, 2, t, exact) : nullptr;
+      t = best_depth_leq(p.shape_id, D, t, exact);
+      k = t ? find_tb(p.shape_id, D, t, exact) : nullptr;
     }
     if (!k) {
       tb_ok = false;
     } else {
       long long full = steps / t;
       long long rem = steps % t;
-      if (full > 0) stages.push_back({KID_STREAM2D, k, (int)full});
+      const int kid = D == 2 ? KID_STREAM2D : KID_STREAM3D;
+      if (full > 0) stages.push_back({kid, k, (int)full});
       while (rem > 0) {
-        const int t2 = best_depth_leq(p.shape_id, 2, (int)rem, exact);
+        const int t2 = best_depth_leq(p.shape_id, D, (int)rem, exact);
         if (t2 == 0) {
           stages.push_back({KID_NAIVE, nullptr, (int)rem});
           break;
         }
         const long long e2 = rem / t2;
-        stages.push_back({KID_STREAM2D, find_tb(p.shape_id, 2, t2, exact), (int)e2});
+        stages.push_back({kid, find_tb(p.shape_id, D, t2, exact), (int)e2});
         rem -= e2 * t2;
       }
     }
@@ -457,20 +616,24 @@ int run_device_impl(const ProblemDesc& p, const double* d_in, double* d_out, dou
       src = (s.epochs % 2 == 1) ? dst : (dst == BUF_OUT ? BUF_SCR : BUF_OUT);
     } else {
       {
-        // every 2-D instantiation loads one 32*C-column row per TMA box
-        const long long dims_ff[2] = {p.ext[1], p.ext[0]};
-        const int box[2] = {s.k->box0, 1};
+        // 2-D: one 32*C-column row per TMA box; 3-D: one LY x LX tile plane
+        const long long dims_ff[3] = {p.ext[D - 1], p.ext[D - 2], D == 3 ? p.ext[0] : 1};
+        const int box[3] = {s.k->box0, s.k->box1, 1};
         for (int i = 0; i < 3 && !result; ++i) {
           if (!bufs[i]) {
             memset(&maps[i], 0, sizeof(CUtensorMap));
             continue;
           }
-          result = encode_map(&maps[i], bufs[i], 2, dims_ff, box);
+          result = encode_map(&maps[i], bufs[i], D, dims_ff, box);
         }
         if (result) break;
       }
-      result = run_tb2d_stage(p, s.k, s.epochs, src, dst, bufs, maps, coop,
-                              prm ? prm->seg_rows : 0, di, st, ctr);
+      if (D == 2)
+        result = run_tb2d_stage(p, s.k, s.epochs, src, dst, bufs, maps, coop,
+                                prm ? prm->seg_rows : 0, di, st, ctr);
+      else
+        result = run_tb3d_stage(p, s.k, s.epochs, src, dst, bufs, maps, coop,
+                                prm ? prm->seg_rows : 0, di, st, ctr);
       if (result) break;
       src = (s.epochs % 2 == 1) ? dst : (dst == BUF_OUT ? BUF_SCR : BUF_OUT);
     }
@@ -525,6 +688,7 @@ static void fill_trace(ebisu_trace* tr, const ProblemDesc& p, long long steps, c
   tr->gm_loads = c.gm_loads;
   tr->gm_stores = c.gm_stores;
   tr->syncs_device = c.syncs_device;
+  tr->syncs_block = c.syncs_block;
   tr->cells_computed = c.cells_computed;
   tr->cells_valid = (uint64_t)interior * (uint64_t)steps;
   tr->device_tiles = c.device_tiles;

@@ -41,6 +41,7 @@ struct TbLaunch {
   // geometry
   int n0, n1, n2;  // extents (2-D: n2 unused)
   int nstrips, nseg, seg_len;  // 2-D decomposition
+  int aligned;                 // 2-D: edge-aligned strips
   int ntx, nty;                // 3-D decomposition (tiles along axis 2 / axis 1)
   int epochs;
   int first_src, first_dst;
@@ -50,6 +51,8 @@ struct TbLaunch {
   int grid;
   bool cooperative;
   cudaStream_t stream;
+  long long* unit_clock;  // optional per-unit timing (profiling)
+  int* work;              // per-epoch dynamic-scheduling counters (device)
 };
 
 struct TbKernel {

@@ -5,26 +5,32 @@
 // through a circular multi-queue, fuses t levels, stores only the core) with
 // a B200 design:
 //
-//  * Work unit = (warp strip, row segment).  A warp strip is 32*C columns
-//    loaded, VW = 32*C - 2*T*R of them valid after T fused levels; row
-//    segments split axis 0 so that >= 148 SMs x resident warps have work
-//    (SURVEY.md §7 hard part 3).  Every warp is an autonomous overlapped
-//    tile: no __syncthreads and no cross-warp traffic inside an epoch.
+//  * Work unit = (warp strip, row segment).  A warp strip is LC = 32*C
+//    columns loaded, VW = LC - 2*HX of them valid after T fused levels
+//    (HX = T*R rounded up to even); row segments split axis 0 so that every
+//    resident warp has work (SURVEY.md §7 hard part 3).  Every warp is an
+//    autonomous overlapped tile: no __syncthreads, no cross-warp traffic
+//    inside an epoch.
 //  * Rows move HBM -> shared memory by TMA (cp.async.bulk.tensor.2d, one
-//    32*C-double box per row; out-of-bounds columns are zero-filled) into a
+//    LC-double box per row; out-of-bounds columns are zero-filled) into a
 //    per-warp S-slot mbarrier ring: the circular multi-queue of
 //    multiqueue.py:103-211 with power-of-two slots and mask addressing.
-//  * Each lane owns C consecutive columns.  The T levels are kept as
-//    register windows of 2R+1 rows per level (the "RST" register streaming
-//    of engine/rst.py, taken to its limit): level s at advance k consumes
-//    rows k-(s+1)R .. k-(s-1)R of level s-1 and emits row k-sR.  The advance
-//    loop is unrolled by 2R+1 so window slots are compile-time registers
-//    (no moves).  Horizontal neighbours outside the lane come from warp
-//    shuffles.
+//  * Each lane owns C consecutive columns.  The T levels are register
+//    windows of 2R+1 rows per level (the "RST" register streaming of
+//    engine/rst.py, taken to its limit): level s at advance k consumes rows
+//    k-(s+1)R .. k-(s-1)R of level s-1 and emits row k-sR.  The advance loop
+//    is unrolled by 2R+1 so window slots are compile-time registers.
+//    Horizontal neighbours outside the lane come from warp shuffles.
 //  * Dirichlet frame (distance < R from a face): a frame cell at level s
-//    equals its value at level s-1, i.e. the centre of the window -- no
-//    stored copy of the input is needed (common.py:96-112 semantics).
-//  * Level T rows are stored straight to HBM for the valid core columns.
+//    equals its value at level s-1 (the window centre), common.py:96-112.
+//    Strip geometry is aligned to the domain edges -- strip 0 starts at
+//    column 0, the last strip ends at column n1 -- so frame columns only ever
+//    sit in lane 0's first R cells or lane 31's last R cells (2R predicated
+//    selects per level, edge strips only); frame rows only occur in the
+//    first/last unrolled blocks of the top/bottom segment, which run a
+//    select variant of the block.  Interior work carries no frame logic, so
+//    edge units cost the same as interior ones and no epoch waits on them.
+//  * Level T rows are stored straight to HBM for the unit's valid columns.
 //  * Epochs (T fused steps each) run inside one cooperative launch separated
 //    by grid.sync(), or one launch per epoch.
 //
@@ -33,6 +39,8 @@
 #pragma once
 
 #include <cooperative_groups.h>
+
+#include <type_traits>
 
 #include "ebisu_common.cuh"
 #include "ebisu_shapes.cuh"
@@ -47,7 +55,10 @@ struct Stream2DArgs {
   int epochs;        // fused epochs in this launch
   int first_src;     // BufId of epoch 0's source
   int first_dst;     // BufId of epoch 0's destination
+  int aligned;       // 1: edge-aligned strips (n1 >= 2*LC); 0: generic strips
   double* buf[3];    // device pointers by BufId
+  long long* unit_clock;  // optional profiling: [units][2] start/end globaltimer (ns)
+  int* work;         // per-epoch unit counters (dynamic scheduling), zeroed by the host
 };
 
 template <class SH, int T, int C, int NW, int S>
@@ -67,6 +78,52 @@ struct Stream2DCfg {
   static_assert(LC <= 256, "TMA box inner dimension is limited to 256 elements");
 };
 
+// Strip geometry shared by host and device.  Aligned mode (n1 >= 2*LC):
+//   strip 0      X0 = 0,          valid [0, VW+HX)
+//   strip j      X0 = j*VW,       valid [j*VW+HX, (j+1)*VW+HX) clipped at xl
+//   last strip   X0 = n1-LC,      valid [xl, n1),  xl = n1-LC+HX
+// Generic mode: X0 = j*VW-HX, valid [j*VW, (j+1)*VW) clipped at n1.
+struct StripGeom {
+  int X0, vlo, vhi;
+  int fc;  // frame columns: 0 none, 1 lane-0 left, 2 lane-31 right, 3 generic
+};
+
+__host__ __device__ inline int stream2d_nstrips(int n1, int LC, int VW, int HX, int R, int C,
+                                                int* aligned) {
+  if (n1 >= 2 * LC && R <= C) {
+    *aligned = 1;
+    const int mid = n1 - LC - VW;  // columns [VW+HX, n1-LC+HX) for middle strips
+    return 2 + (mid > 0 ? (mid + VW - 1) / VW : 0);
+  }
+  *aligned = 0;
+  return (n1 + VW - 1) / VW;
+}
+
+__host__ __device__ inline StripGeom stream2d_strip(int j, int nstrips, int aligned, int n1,
+                                                    int LC, int VW, int HX) {
+  StripGeom g;
+  if (aligned) {
+    const int xl = n1 - LC + HX;
+    if (j == nstrips - 1) {
+      g.X0 = n1 - LC;
+      g.vlo = xl;
+      g.vhi = n1;
+      g.fc = 2;
+    } else {
+      g.X0 = j * VW;
+      g.vlo = j == 0 ? 0 : j * VW + HX;
+      g.vhi = min((j + 1) * VW + HX, xl);
+      g.fc = j == 0 ? 1 : 0;
+    }
+  } else {
+    g.X0 = j * VW - HX;
+    g.vlo = j * VW;
+    g.vhi = min((j + 1) * VW, n1);
+    g.fc = 3;
+  }
+  return g;
+}
+
 // Does any tap in row dy have a nonzero column offset?
 template <class SH>
 __host__ __device__ constexpr bool row_has_halo(int dy) {
@@ -80,23 +137,21 @@ __host__ __device__ constexpr int pmod(int a) {
   return ((a % W) + W) % W;
 }
 
-// One work unit (warp strip x row segment) of one epoch.  EDGE = the unit
-// owns frame cells (top/bottom segment, first/last strip): only then are the
-// frame-row branches and frame-column selects compiled in; interior units run
-// the pure tap pipeline.
-template <class SH, int T, int C, int S, bool EXACT, bool EDGE>
+// One work unit (warp strip x row segment) of one epoch.  FC selects the
+// frame-column handling (see StripGeom); frame rows are handled per block.
+template <class SH, int T, int C, int S, bool EXACT, int FC>
 __device__ __forceinline__ void stream2d_unit(const CUtensorMap* tm, double* __restrict__ out,
                                               double* ring, uint64_t* bars, uint32_t ring_cnt,
-                                              int lane, int n0, int n1, int X0, int r0, int r1,
-                                              const Coefs<SH::NT>& cf) {
+                                              int lane, int n0, int n1, const StripGeom& g,
+                                              int r0, int r1, const Coefs<SH::NT>& cf) {
   constexpr int R = SH::R;
   constexpr int W = 2 * R + 1;
   constexpr int LC = 32 * C;
   constexpr int ROW_BYTES = LC * 8;
   constexpr int TR = T * R;
-  constexpr int HX = (TR + 1) & ~1;
-  constexpr int VW = LC - 2 * HX;
+  static_assert(FC == 0 || FC == 3 || R <= C, "frame columns must fit in one lane");
 
+  const int X0 = g.X0;
   const int ka = max(0, r0 - TR);
   const int kb = min(n0, r1 + TR);
   const int kend = r1 + TR;
@@ -110,15 +165,25 @@ __device__ __forceinline__ void stream2d_unit(const CUtensorMap* tm, double* __r
     }
   }
 
-  bool fcol[C];   // frame column (EDGE only)
-  bool stcol[C];  // stored (valid core) column
+  bool fcol[C];   // this lane's frame columns
+  bool stcol[C];  // stored (valid) columns
 #pragma unroll
   for (int c = 0; c < C; ++c) {
-    const int lc = lane * C + c;
-    const int x = X0 + lc;
-    fcol[c] = EDGE && ((x < R) || (x >= n1 - R));
-    stcol[c] = (lc >= HX) && (lc < HX + VW) && (x < n1);
+    const int x = X0 + lane * C + c;
+    if constexpr (FC == 1)
+      fcol[c] = (c < R) && (lane == 0);
+    else if constexpr (FC == 2)
+      fcol[c] = (c >= C - R) && (lane == 31);
+    else if constexpr (FC == 3)
+      fcol[c] = (x < R) || (x >= n1 - R);
+    else
+      fcol[c] = false;
+    stcol[c] = (x >= g.vlo) && (x < g.vhi);
   }
+  // compile-time: which columns may hold frame cells
+  auto col_may_frame = [](int c) constexpr {
+    return FC == 3 || (FC == 1 && c < R) || (FC == 2 && c >= C - R);
+  };
 
   double win[T][W][C];
 #pragma unroll
@@ -128,7 +193,10 @@ __device__ __forceinline__ void stream2d_unit(const CUtensorMap* tm, double* __r
 #pragma unroll
       for (int c = 0; c < C; ++c) win[s][w][c] = 0.0;
 
-  for (int kbase = ka; kbase < kend; kbase += W) {
+  // One unrolled block of W advances.  FROWS: some target row in this block
+  // may be a frame row (only near the top/bottom of the grid).
+  auto block = [&](int kbase, auto frows_tag) {
+    constexpr bool FROWS = decltype(frows_tag)::value;
 #pragma unroll
     for (int uu = 0; uu < W; ++uu) {
       const int k = kbase + uu;
@@ -177,58 +245,62 @@ __device__ __forceinline__ void stream2d_unit(const CUtensorMap* tm, double* __r
       static_for<T>([&](auto sI) {
         constexpr int s = decltype(sI)::value + 1;  // level being produced
         const int q = k - s * R;                    // its target row
-        double nv[C];
-        bool frame_row = false;
-        if constexpr (EDGE) frame_row = (q < R) || (q >= n0 - R);
-        if (frame_row) {
-          // frame row (or warm-up row outside the grid): value carries over
-#pragma unroll
-          for (int c = 0; c < C; ++c) nv[c] = win[s - 1][pmod<W>(uu - s * R)][c];
-        } else {
-          // horizontal halos (only rows whose taps leave the lane's columns)
-          double hl[W][R], hr[W][R];
-          static_for<W>([&](auto wI) {
-            constexpr int dy = decltype(wI)::value - R;
-            if constexpr (row_has_halo<SH>(dy)) {
-              static_for<R>([&](auto jI) {
-                constexpr int j = decltype(jI)::value;
-                constexpr int ccl = -R + j;
-                constexpr int dl = (-ccl + C - 1) / C;
-                constexpr int coll = ccl + dl * C;
-                constexpr int ccr = C + j;
-                constexpr int dr = ccr / C;
-                constexpr int colr = ccr - dr * C;
-                const int sl = pmod<W>(uu - s * R + dy);
-                hl[wI][j] = __shfl_up_sync(kFullMask, win[s - 1][sl][coll], dl);
-                hr[wI][j] = __shfl_down_sync(kFullMask, win[s - 1][sl][colr], dr);
-              });
-            }
-          });
+        // horizontal halos (only rows whose taps leave the lane's columns)
+        double hl[W][R], hr[W][R];
+        static_for<W>([&](auto wI) {
+          constexpr int dy = decltype(wI)::value - R;
+          if constexpr (row_has_halo<SH>(dy)) {
+            static_for<R>([&](auto jI) {
+              constexpr int j = decltype(jI)::value;
+              constexpr int ccl = -R + j;
+              constexpr int dl = (-ccl + C - 1) / C;
+              constexpr int coll = ccl + dl * C;
+              constexpr int ccr = C + j;
+              constexpr int dr = ccr / C;
+              constexpr int colr = ccr - dr * C;
+              const int sl = pmod<W>(uu - s * R + dy);
+              hl[wI][j] = __shfl_up_sync(kFullMask, win[s - 1][sl][coll], dl);
+              hr[wI][j] = __shfl_down_sync(kFullMask, win[s - 1][sl][colr], dr);
+            });
+          }
+        });
+        // tap-major order: the C per-column chains are independent
+        double acc[C];
+        static_for<SH::NT>([&](auto iI) {
+          constexpr int i = decltype(iI)::value;
+          constexpr Off o = SH::tap(i);
 #pragma unroll
           for (int c = 0; c < C; ++c) {
-            double acc = 0.0;
-            static_for<SH::NT>([&](auto iI) {
-              constexpr int i = decltype(iI)::value;
-              constexpr Off o = SH::tap(i);
-              const int sl = pmod<W>(uu - s * R + o.d0);
-              const int cc = c + o.d1;
-              double x;
-              if (cc < 0)
-                x = hl[o.d0 + R][cc + R];
-              else if (cc >= C)
-                x = hr[o.d0 + R][cc - C];
-              else
-                x = win[s - 1][sl][cc];
-              if constexpr (i == 0)
-                acc = tap_first<EXACT>(cf.c[0], x);
-              else
-                acc = tap_next<EXACT>(acc, cf.c[i], x);
-            });
-            if constexpr (EDGE)
-              nv[c] = fcol[c] ? win[s - 1][pmod<W>(uu - s * R)][c] : acc;
+            const int sl = pmod<W>(uu - s * R + o.d0);
+            const int cc = c + o.d1;
+            double x;
+            if (cc < 0)
+              x = hl[o.d0 + R][cc + R];
+            else if (cc >= C)
+              x = hr[o.d0 + R][cc - C];
             else
-              nv[c] = acc;
+              x = win[s - 1][sl][cc];
+            if constexpr (i == 0)
+              acc[c] = tap_first<EXACT>(cf.c[0], x);
+            else
+              acc[c] = tap_next<EXACT>(acc[c], cf.c[i], x);
           }
+        });
+        // frame cells carry level s-1's centre (branch-free selects)
+        double nv[C];
+        bool frow = false;
+        if constexpr (FROWS) frow = (q < R) || (q >= n0 - R);
+#pragma unroll
+        for (int c = 0; c < C; ++c) {
+          const double centre = win[s - 1][pmod<W>(uu - s * R)][c];
+          if (FROWS && col_may_frame(c))
+            nv[c] = (frow || fcol[c]) ? centre : acc[c];
+          else if (FROWS)
+            nv[c] = frow ? centre : acc[c];
+          else if (col_may_frame(c))
+            nv[c] = fcol[c] ? centre : acc[c];
+          else
+            nv[c] = acc[c];
         }
         if constexpr (s < T) {
 #pragma unroll
@@ -243,7 +315,23 @@ __device__ __forceinline__ void stream2d_unit(const CUtensorMap* tm, double* __r
         }
       });
     }
+  };
+
+  for (int kbase = ka; kbase < kend; kbase += W) {
+    // target rows of this block: [kbase - TR, kbase + W - 1 - R]
+    const bool frows = (kbase - TR < R) || (kbase + W - 1 >= n0);
+    if (frows)
+      block(kbase, std::true_type{});
+    else
+      block(kbase, std::false_type{});
   }
+}
+
+// Warp-wide atomic grab of the next work unit (lane 0 increments).
+__device__ __forceinline__ int next_unit(int* counter, int lane) {
+  int u = 0;
+  if (lane == 0) u = atomicAdd(counter, 1);
+  return __shfl_sync(kFullMask, u, 0);
 }
 
 template <class SH, int T, int C, int NW, int S, bool EXACT, int MINB>
@@ -252,9 +340,7 @@ __global__ void __launch_bounds__(NW * 32, MINB)
                const __grid_constant__ Coefs<SH::NT> cf) {
   using Cfg = Stream2DCfg<SH, T, C, NW, S>;
   constexpr int R = Cfg::R;
-  constexpr int VW = Cfg::VW;
   constexpr int TR = T * R;
-  constexpr int HX = Cfg::HX;
 
   extern __shared__ __align__(1024) unsigned char smem[];
   const int warp = threadIdx.x >> 5;
@@ -273,8 +359,6 @@ __global__ void __launch_bounds__(NW * 32, MINB)
   __syncwarp();
 
   const int n0 = a.n0, n1 = a.n1;
-  const int gwarp = blockIdx.x * NW + warp;
-  const int nwarps = gridDim.x * NW;
   const int units = a.nstrips * a.nseg;
   uint32_t ring_cnt = 0;  // rows consumed so far by this warp (ring position)
 
@@ -283,25 +367,49 @@ __global__ void __launch_bounds__(NW * 32, MINB)
     const CUtensorMap* tm = &maps.m[src];
     double* __restrict__ out = (dst == BUF_OUT) ? a.buf[BUF_OUT] : a.buf[BUF_SCR];
 
-    for (int u = gwarp; u < units; u += nwarps) {
+    // Dynamic unit distribution: a warp grabs the next unit when it finishes
+    // one, so warps the scheduler favours take more units and the epoch tail
+    // is at most one unit (static assignment left SMs half idle).
+    for (int u = next_unit(a.work + e, lane); u < units; u = next_unit(a.work + e, lane)) {
       const int strip = u % a.nstrips;
       const int seg = u / a.nstrips;
-      const int X0 = strip * VW - HX;  // global column of loaded column 0 (even)
+      const StripGeom g =
+          stream2d_strip(strip, a.nstrips, a.aligned, n1, Cfg::LC, Cfg::VW, Cfg::HX);
       const int r0 = seg * a.seg_len;
       const int r1 = min(n0, r0 + a.seg_len);
       const int ka = max(0, r0 - TR);
       const int kb = min(n0, r1 + TR);
-      // Frame cells inside this unit's dependency cone (valid range +- T*R)?
-      // Only then must frame rows/columns be carried instead of computed.
-      const bool edge = (r0 - TR < R) || (r1 + TR > n0 - R) || (strip * VW - TR < R) ||
-                        ((strip + 1) * VW + TR > n1 - R);
-      if (__shfl_sync(kFullMask, edge, 0))
-        stream2d_unit<SH, T, C, S, EXACT, true>(tm, out, ring, bars, ring_cnt, lane, n0, n1,
-                                                X0, r0, r1, cf);
-      else
-        stream2d_unit<SH, T, C, S, EXACT, false>(tm, out, ring, bars, ring_cnt, lane, n0, n1,
-                                                 X0, r0, r1, cf);
+      long long t_start = 0;
+      if (a.unit_clock && e == 0 && lane == 0)
+        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_start));
+      if constexpr (R > C) {
+        stream2d_unit<SH, T, C, S, EXACT, 3>(tm, out, ring, bars, ring_cnt, lane, n0, n1, g, r0,
+                                             r1, cf);
+      } else switch (g.fc) {
+        case 0:
+          stream2d_unit<SH, T, C, S, EXACT, 0>(tm, out, ring, bars, ring_cnt, lane, n0, n1, g,
+                                               r0, r1, cf);
+          break;
+        case 1:
+          stream2d_unit<SH, T, C, S, EXACT, 1>(tm, out, ring, bars, ring_cnt, lane, n0, n1, g,
+                                               r0, r1, cf);
+          break;
+        case 2:
+          stream2d_unit<SH, T, C, S, EXACT, 2>(tm, out, ring, bars, ring_cnt, lane, n0, n1, g,
+                                               r0, r1, cf);
+          break;
+        default:
+          stream2d_unit<SH, T, C, S, EXACT, 3>(tm, out, ring, bars, ring_cnt, lane, n0, n1, g,
+                                               r0, r1, cf);
+          break;
+      }
       ring_cnt += (uint32_t)(kb - ka);
+      if (a.unit_clock && e == 0 && lane == 0) {
+        long long t_end;
+        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_end));
+        a.unit_clock[2 * u] = t_start;
+        a.unit_clock[2 * u + 1] = t_end;
+      }
     }
 
     if (e + 1 < a.epochs) {

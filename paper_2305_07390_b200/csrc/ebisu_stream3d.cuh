@@ -1,0 +1,413 @@
+// ebisu_stream3d.cuh -- 3-D (2.5-D streaming) temporal-blocking sweep, sm_100a.
+//
+// Replaces the reference's 3-D engines (engine/sm.py:95-206 plane pipeline
+// over a circular multi-queue; engine/device.py:292-389 streamed device
+// tiles with per-level halo exchange and a barrier per advance) with:
+//
+//  * Work unit = (tile ty, tile tx, z segment).  The CTA owns an LY x LX
+//    in-plane tile (LY = NWY*CY rows along axis 1, LX = 32*CX columns along
+//    axis 2) and streams it along axis 0.  Planes arrive by TMA
+//    (cp.async.bulk.tensor.3d, box {LX, LY, 1}, out-of-bounds zero fill) in an
+//    S-slot mbarrier ring.
+//  * Thread (warp w, lane l) owns the CY x CX block rows w*CY.., columns
+//    l*CX..; its z-window of every level lives in registers (RST register
+//    streaming).  In-plane neighbours come from a per-level shared-memory
+//    plane buffer that each level writes once per advance ("push halo"), read
+//    one or more advances later ("pull halo"), with ONE __syncthreads per
+//    advance (the reference's lazy mode: one barrier per advance,
+//    device.py:381-387).
+//  * Skew Z between levels: level s at advance k emits plane k - s*Z.  For
+//    stars only the centre plane needs in-plane neighbours, so Z = R; for
+//    boxes every plane does, so Z = R + 1.  Either way every in-plane value a
+//    level reads was produced in an earlier advance.
+//  * Frame cells carry the previous level's centre (EDGE units only).
+//  * Exact mode: __dmul_rn/__dadd_rn in catalog tap order (bitwise).
+#pragma once
+
+#include <cooperative_groups.h>
+
+#include "ebisu_common.cuh"
+#include "ebisu_shapes.cuh"
+
+namespace ebisu {
+
+struct Stream3DArgs {
+  int n0, n1, n2;   // extents; plane pitch n1*n2, row pitch n2
+  int nty, ntx;     // tiles along axis 1 / axis 2
+  int nseg;         // z segments
+  int seg_len;
+  int epochs;
+  int first_src, first_dst;
+  double* buf[3];
+  int* work;  // per-epoch unit counters (dynamic scheduling), zeroed by the host
+};
+
+// Does tap set need in-plane neighbours on planes other than the centre?
+template <class SH>
+__host__ __device__ constexpr bool offcentre_inplane() {
+  for (int i = 0; i < SH::NT; ++i)
+    if (SH::tap(i).d0 != 0 && (SH::tap(i).d1 != 0 || SH::tap(i).d2 != 0)) return true;
+  return false;
+}
+
+// DEC = decoupled levels: skew R+1 even for stars, so that within one
+// advance no level consumes another level's output (T independent chains).
+// Which planes (dz) of the window need values outside the thread's block?
+template <class SH>
+__host__ __device__ constexpr bool plane_needs_inplane(int dz) {
+  for (int i = 0; i < SH::NT; ++i)
+    if (SH::tap(i).d0 == dz && (SH::tap(i).d1 != 0 || SH::tap(i).d2 != 0)) return true;
+  return false;
+}
+
+// Does extended row ey (relative to the block, in [-R, CY+R)) of plane dz
+// need x-halo values (some tap reaches (ey, outside the lane's columns))?
+template <class SH>
+__host__ __device__ constexpr bool row_needs_x_halo(int dz, int ey, int CY) {
+  for (int i = 0; i < SH::NT; ++i) {
+    const Off o = SH::tap(i);
+    if (o.d0 != dz || o.d2 == 0) continue;
+    // cell rows cy in [0, CY) reach ey = cy + d1
+    if (ey - o.d1 >= 0 && ey - o.d1 < CY) return true;
+  }
+  return false;
+}
+
+template <class SH, int T, int CY, int CX, int NWY, int S, bool DEC = false>
+struct Stream3DCfg {
+  static constexpr int R = SH::R;
+  static constexpr int Z = (offcentre_inplane<SH>() || DEC) ? R + 1 : R;  // level skew
+  static constexpr int WN = 2 * R + (Z - R) + 1;                   // window planes
+  static constexpr int NB = offcentre_inplane<SH>() ? Z + R + 1 : Z + 1;  // halo buffers
+  static constexpr int LY = NWY * CY;
+  static constexpr int LX = 32 * CX;
+  static constexpr int HY = T * R;
+  static constexpr int HX = (T * R + 1) & ~1;  // TMA: 16-byte aligned box start
+  static constexpr int VY = LY - 2 * HY;
+  static constexpr int VX = LX - 2 * HX;
+  // Halo buffer: per warp, its top R and bottom R rows of a level's plane
+  // ("push halo"); neighbours along axis 2 come from warp shuffles.
+  static constexpr int HROWW = 2 * R;                 // rows per warp
+  static constexpr int HPLANE = NWY * HROWW * LX;     // doubles per halo buffer
+  static constexpr int RING_PLANE = LY * LX;          // doubles per ring slot
+  static constexpr int RING_BYTES = S * RING_PLANE * 8;
+  static constexpr int HALO_BYTES = T * NB * HPLANE * 8;
+  static constexpr int SMEM_BYTES = RING_BYTES + HALO_BYTES + S * 8;
+  static_assert(CY >= R, "a warp's rows must cover the radius");
+  static_assert(VY > 0 && VX > 0, "tile leaves no valid core");
+  static_assert(LX <= 256 && LY <= 256, "TMA box dims are limited to 256");
+  static_assert((S & (S - 1)) == 0, "ring slots must be a power of two");
+  static_assert(SMEM_BYTES <= 227 * 1024, "shared memory budget");
+};
+
+template <class SH, int T, int CY, int CX, int NWY, int S, bool DEC, bool EXACT, bool EDGE>
+__device__ __forceinline__ void stream3d_unit(const CUtensorMap* tm, double* __restrict__ out,
+                                              double* ring, double* halo, uint64_t* bars,
+                                              uint32_t ring_cnt, int warp, int lane, int n0,
+                                              int n1, int n2, int X0, int Y0, int r0, int r1,
+                                              const Coefs<SH::NT>& cf) {
+  using Cfg = Stream3DCfg<SH, T, CY, CX, NWY, S, DEC>;
+  constexpr int R = Cfg::R, Z = Cfg::Z, WN = Cfg::WN, NB = Cfg::NB;
+  constexpr int LY = Cfg::LY, LX = Cfg::LX, HY = Cfg::HY, HX = Cfg::HX;
+  constexpr int PLANE_BYTES = LY * LX * 8;
+  constexpr int TZ = T * Z;  // pipeline depth along z
+
+  const int ka = max(0, r0 - T * R);
+  const int kb = min(n0, r1 + T * R);
+  const int kend = r1 + TZ;
+  const int tid = warp * 32 + lane;
+  const int ty0 = warp * CY;  // tile row of this thread's first row
+  const int tx0 = lane * CX;  // tile column of this thread's first column
+
+  if (tid == 0) {
+    for (int i = 0; i < S && ka + i < kb; ++i) {
+      const uint32_t slot = (ring_cnt + i) & (S - 1);
+      mbar_arrive_expect_tx(&bars[slot], PLANE_BYTES);
+      tma_load_3d(ring + slot * Cfg::RING_PLANE, tm, X0, Y0, ka + i, &bars[slot]);
+    }
+  }
+
+  bool fcell[CY][CX];
+  bool stcell[CY][CX];
+#pragma unroll
+  for (int cy = 0; cy < CY; ++cy)
+#pragma unroll
+    for (int cx = 0; cx < CX; ++cx) {
+      const int yy = Y0 + ty0 + cy, xx = X0 + tx0 + cx;
+      fcell[cy][cx] = EDGE && ((yy < R) || (yy >= n1 - R) || (xx < R) || (xx >= n2 - R));
+      stcell[cy][cx] = (ty0 + cy >= HY) && (ty0 + cy < LY - HY) && (tx0 + cx >= HX) &&
+                       (tx0 + cx < LX - HX) && (yy < n1) && (xx < n2);
+    }
+
+  double win[T][WN][CY][CX];
+#pragma unroll
+  for (int s = 0; s < T; ++s)
+#pragma unroll
+    for (int w = 0; w < WN; ++w)
+#pragma unroll
+      for (int cy = 0; cy < CY; ++cy)
+#pragma unroll
+        for (int cx = 0; cx < CX; ++cx) win[s][w][cy][cx] = 0.0;
+
+  // Halo buffer (level, b): warp-major [NWY][2R][LX]; this thread's columns.
+  auto hrow = [&](int level, int b, int w, int r) -> double* {
+    return halo + (size_t)(level * NB + b) * Cfg::HPLANE + (size_t)(w * 2 * R + r) * LX + tx0;
+  };
+  // push: top R rows and bottom R rows of this thread's block
+  auto push = [&](int level, int b, const double (&v)[CY][CX]) {
+    static_for<2 * R>([&](auto rI) {
+      constexpr int r = decltype(rI)::value;
+      constexpr int cy = r < R ? r : CY - 2 * R + r;
+      double* d = hrow(level, b, warp, r);
+      if constexpr (CX % 2 == 0) {
+#pragma unroll
+        for (int cx = 0; cx < CX; cx += 2)
+          *reinterpret_cast<double2*>(d + cx) = make_double2(v[cy][cx], v[cy][cx + 1]);
+      } else {
+#pragma unroll
+        for (int cx = 0; cx < CX; ++cx) d[cx] = v[cy][cx];
+      }
+    });
+  };
+  // pull: rows above (the warp above's bottom rows) and below (the warp
+  // below's top rows).  Edge warps of the tile read their own buffer rows:
+  // those cells lie outside the tile's valid core anyway.
+  const int wa = warp > 0 ? warp - 1 : warp;
+  const int wbl = warp < NWY - 1 ? warp + 1 : warp;
+
+  for (int kbase = ka; kbase < kend; kbase += WN) {
+#pragma unroll
+    for (int uu = 0; uu < WN; ++uu) {
+      const int k = kbase + uu;
+      const int bk = k % NB;  // halo buffer written this advance
+      // ---- level 0 ----------------------------------------------------------
+      {
+        double v[CY][CX];
+        if (k < kb) {
+          const uint32_t pos = ring_cnt + (uint32_t)(k - ka);
+          const uint32_t slot = pos & (S - 1);
+          mbar_wait(&bars[slot], (pos / S) & 1);
+          const double* p = ring + slot * Cfg::RING_PLANE + ty0 * LX + tx0;
+#pragma unroll
+          for (int cy = 0; cy < CY; ++cy) {
+            if constexpr (CX % 2 == 0) {
+#pragma unroll
+              for (int cx = 0; cx < CX; cx += 2) {
+                const double2 t2 = *reinterpret_cast<const double2*>(p + cy * LX + cx);
+                v[cy][cx] = t2.x;
+                v[cy][cx + 1] = t2.y;
+              }
+            } else {
+#pragma unroll
+              for (int cx = 0; cx < CX; ++cx) v[cy][cx] = p[cy * LX + cx];
+            }
+          }
+        } else {
+#pragma unroll
+          for (int cy = 0; cy < CY; ++cy)
+#pragma unroll
+            for (int cx = 0; cx < CX; ++cx) v[cy][cx] = 0.0;
+        }
+#pragma unroll
+        for (int cy = 0; cy < CY; ++cy)
+#pragma unroll
+          for (int cx = 0; cx < CX; ++cx) win[0][uu][cy][cx] = v[cy][cx];
+        push(0, bk, v);
+      }
+      // ---- levels 1..T --------------------------------------------------------
+      static_for<T>([&](auto sI) {
+        constexpr int s = decltype(sI)::value + 1;
+        const int q = k - s * Z;  // target plane of level s
+        double nv[CY][CX];
+        // frame plane / frame cell: value carries over from level s-1 (selects,
+        // not branches, so all levels stay in one basic block)
+        bool frame_plane = false;
+        if constexpr (EDGE) frame_plane = (q < R) || (q >= n0 - R);
+        {
+          // extended neighbourhood of the planes that need in-plane values:
+          // ext[dz][cy+R][cx+R], cy in [-R, CY+R), cx in [-R, CX+R)
+          double ext[2 * R + 1][CY + 2 * R][CX + 2 * R];
+          static_for<2 * R + 1>([&](auto zI) {
+            constexpr int dz = decltype(zI)::value - R;
+            if constexpr (plane_needs_inplane<SH>(dz)) {
+              const int sl = pmod<WN>(uu - s * Z + dz);
+              const int b = (k - Z + dz + NB * 4) % NB;  // written at advance k - Z + dz
+#pragma unroll
+              for (int cy = 0; cy < CY; ++cy)
+#pragma unroll
+                for (int cx = 0; cx < CX; ++cx) ext[zI][cy + R][cx + R] = win[s - 1][sl][cy][cx];
+              // rows above / below from the halo buffer
+#pragma unroll
+              for (int r = 0; r < R; ++r) {
+                const double* up = hrow(s - 1, b, wa, warp > 0 ? R + r : r);
+                const double* dn = hrow(s - 1, b, wbl, warp < NWY - 1 ? r : R + r);
+                if constexpr (CX % 2 == 0) {
+#pragma unroll
+                  for (int cx = 0; cx < CX; cx += 2) {
+                    const double2 a2 = *reinterpret_cast<const double2*>(up + cx);
+                    const double2 b2 = *reinterpret_cast<const double2*>(dn + cx);
+                    ext[zI][r][cx + R] = a2.x;
+                    ext[zI][r][cx + 1 + R] = a2.y;
+                    ext[zI][CY + R + r][cx + R] = b2.x;
+                    ext[zI][CY + R + r][cx + 1 + R] = b2.y;
+                  }
+                } else {
+#pragma unroll
+                  for (int cx = 0; cx < CX; ++cx) {
+                    ext[zI][r][cx + R] = up[cx];
+                    ext[zI][CY + R + r][cx + R] = dn[cx];
+                  }
+                }
+              }
+              // columns left / right from the neighbouring lanes
+#pragma unroll
+              for (int ey = 0; ey < CY + 2 * R; ++ey) {
+                if (!row_needs_x_halo<SH>(dz, ey - R, CY)) continue;
+#pragma unroll
+                for (int j = 0; j < R; ++j) {
+                  const int ccl = -R + j;
+                  const int dl = (-ccl + CX - 1) / CX;
+                  const int coll = ccl + dl * CX;
+                  ext[zI][ey][j] = __shfl_up_sync(kFullMask, ext[zI][ey][coll + R], dl);
+                  const int ccr = CX + j;
+                  const int dr = ccr / CX;
+                  const int colr = ccr - dr * CX;
+                  ext[zI][ey][CX + R + j] = __shfl_down_sync(kFullMask, ext[zI][ey][colr + R], dr);
+                }
+              }
+            }
+          });
+          // tap-major: CY*CX independent chains interleave in the instruction stream
+          double acc[CY][CX];
+          static_for<SH::NT>([&](auto iI) {
+            constexpr int i = decltype(iI)::value;
+            constexpr Off o = SH::tap(i);
+#pragma unroll
+            for (int cy = 0; cy < CY; ++cy) {
+#pragma unroll
+              for (int cx = 0; cx < CX; ++cx) {
+                double x;
+                if constexpr (plane_needs_inplane<SH>(o.d0))
+                  x = ext[o.d0 + R][cy + o.d1 + R][cx + o.d2 + R];
+                else
+                  x = win[s - 1][pmod<WN>(uu - s * Z + o.d0)][cy][cx];
+                if constexpr (i == 0)
+                  acc[cy][cx] = tap_first<EXACT>(cf.c[0], x);
+                else
+                  acc[cy][cx] = tap_next<EXACT>(acc[cy][cx], cf.c[i], x);
+              }
+            }
+          });
+#pragma unroll
+          for (int cy = 0; cy < CY; ++cy)
+#pragma unroll
+            for (int cx = 0; cx < CX; ++cx) {
+              if constexpr (EDGE)
+                nv[cy][cx] = (frame_plane || fcell[cy][cx])
+                                 ? win[s - 1][pmod<WN>(uu - s * Z)][cy][cx]
+                                 : acc[cy][cx];
+              else
+                nv[cy][cx] = acc[cy][cx];
+            }
+        }
+        if constexpr (s < T) {
+#pragma unroll
+          for (int cy = 0; cy < CY; ++cy)
+#pragma unroll
+            for (int cx = 0; cx < CX; ++cx) win[s][pmod<WN>(uu - s * Z)][cy][cx] = nv[cy][cx];
+          push(s, bk, nv);
+        } else {
+          if (q >= r0 && q < r1) {
+            const long long base =
+                ((long long)q * n1 + (long long)(Y0 + ty0)) * (long long)n2 + (X0 + tx0);
+#pragma unroll
+            for (int cy = 0; cy < CY; ++cy)
+#pragma unroll
+              for (int cx = 0; cx < CX; ++cx)
+                if (stcell[cy][cx]) out[base + (long long)cy * n2 + cx] = nv[cy][cx];
+          }
+        }
+      });
+      // one barrier per advance: halo pushes visible, ring slot k consumed
+      __syncthreads();
+      if (tid == 0 && k < kb && k + S < kb) {
+        const uint32_t pos = ring_cnt + (uint32_t)(k - ka);
+        const uint32_t slot = pos & (S - 1);
+        mbar_arrive_expect_tx(&bars[slot], PLANE_BYTES);
+        tma_load_3d(ring + slot * Cfg::RING_PLANE, tm, X0, Y0, k + S, &bars[slot]);
+      }
+    }
+  }
+}
+
+template <class SH, int T, int CY, int CX, int NWY, int S, bool DEC, bool EXACT, int MINB>
+__global__ void __launch_bounds__(NWY * 32, MINB)
+    k_stream3d(const __grid_constant__ TmapSet maps, const Stream3DArgs a,
+               const __grid_constant__ Coefs<SH::NT> cf) {
+  using Cfg = Stream3DCfg<SH, T, CY, CX, NWY, S, DEC>;
+  constexpr int R = Cfg::R;
+  extern __shared__ __align__(1024) unsigned char smem[];
+  double* ring = reinterpret_cast<double*>(smem);
+  double* halo = reinterpret_cast<double*>(smem + Cfg::RING_BYTES);
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + Cfg::RING_BYTES + Cfg::HALO_BYTES);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+
+  if (threadIdx.x == 0) {
+#pragma unroll
+    for (int i = 0; i < S; ++i) mbar_init(&bars[i], 1);
+    fence_mbarrier_init();
+    prefetch_tmap(&maps.m[0]);
+    prefetch_tmap(&maps.m[1]);
+    prefetch_tmap(&maps.m[2]);
+  }
+  __syncthreads();
+
+  const int n0 = a.n0, n1 = a.n1, n2 = a.n2;
+  const int units = a.nty * a.ntx * a.nseg;
+  uint32_t ring_cnt = 0;
+  int src = a.first_src, dst = a.first_dst;
+  for (int e = 0; e < a.epochs; ++e) {
+    const CUtensorMap* tm = &maps.m[src];
+    double* __restrict__ out = (dst == BUF_OUT) ? a.buf[BUF_OUT] : a.buf[BUF_SCR];
+    __shared__ int s_unit;
+    for (;;) {
+      // dynamic unit distribution across CTAs (tail <= one unit)
+      if (threadIdx.x == 0) s_unit = atomicAdd(a.work + e, 1);
+      __syncthreads();
+      const int u = s_unit;
+      if (u >= units) break;
+      const int tx = u % a.ntx;
+      const int ty = (u / a.ntx) % a.nty;
+      const int seg = u / (a.ntx * a.nty);
+      const int X0 = tx * Cfg::VX - Cfg::HX;
+      const int Y0 = ty * Cfg::VY - Cfg::HY;
+      const int r0 = seg * a.seg_len;
+      const int r1 = min(n0, r0 + a.seg_len);
+      const int TR = T * R;
+      const bool edge = (r0 - TR < R) || (r1 + TR > n0 - R) || (ty * Cfg::VY - TR < R) ||
+                        ((ty + 1) * Cfg::VY + TR > n1 - R) || (tx * Cfg::VX - TR < R) ||
+                        ((tx + 1) * Cfg::VX + TR > n2 - R);
+      if (edge)
+        stream3d_unit<SH, T, CY, CX, NWY, S, DEC, EXACT, true>(tm, out, ring, halo, bars, ring_cnt,
+                                                          warp, lane, n0, n1, n2, X0, Y0, r0,
+                                                          r1, cf);
+      else
+        stream3d_unit<SH, T, CY, CX, NWY, S, DEC, EXACT, false>(tm, out, ring, halo, bars, ring_cnt,
+                                                           warp, lane, n0, n1, n2, X0, Y0, r0,
+                                                           r1, cf);
+      ring_cnt += (uint32_t)(min(n0, r1 + TR) - max(0, r0 - TR));
+      __syncthreads();  // halo buffers and s_unit are reused by the next unit
+    }
+    if (e + 1 < a.epochs) {
+      fence_proxy_async_global();
+      __threadfence();
+      cooperative_groups::this_grid().sync();
+      fence_proxy_async_global();
+    }
+    const int nsrc = dst;
+    dst = (dst == BUF_OUT) ? BUF_SCR : BUF_OUT;
+    src = nsrc;
+  }
+}
+
+}  // namespace ebisu

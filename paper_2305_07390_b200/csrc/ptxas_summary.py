@@ -1,8 +1,10 @@
-"""Summarise ptxas -v logs: kernel template args, registers, spills."""
-import glob, re, sys, os
-base = sys.argv[1] if len(sys.argv) > 1 else os.path.join(os.path.dirname(__file__), "../../build/csrc")
+"""Summarise ptxas -v logs: demangled kernel, registers, spills."""
+import glob, os, re, subprocess, sys
+
+base = sys.argv[1] if len(sys.argv) > 1 else os.path.join(os.path.dirname(os.path.abspath(__file__)), "../../build/csrc")
+recs = []
 for log in sorted(glob.glob(os.path.join(base, "*.ptxas.log"))):
-    cur = None
+    cur = spill = None
     for line in open(log):
         m = re.search(r"Compiling entry function '(\S+)'", line)
         if m:
@@ -13,7 +15,9 @@ for log in sorted(glob.glob(os.path.join(base, "*.ptxas.log"))):
             spill = m.groups()
         m = re.search(r"Used (\d+) registers", line)
         if m and cur:
-            dm = re.search(r"k_stream2dINS_(\w+?)ILi(\d)ELi(\d)EEELi(\d+)ELi(\d+)ELi(\d+)ELi(\d+)ELb(\d)ELi(\d+)E", cur)
-            name = cur if not dm else f"stream2d {dm.group(1)}<{dm.group(2)},{dm.group(3)}> T={dm.group(4)} C={dm.group(5)} exact={dm.group(8)} minb={dm.group(9)}"
-            print(f"{name:60s} regs={m.group(1):>4s} stack={spill[0]} spill_st={spill[1]} spill_ld={spill[2]}")
+            recs.append((cur, m.group(1), spill))
             cur = None
+names = subprocess.run(["c++filt"], input="\n".join(r[0] for r in recs), capture_output=True, text=True).stdout.splitlines()
+for (mangled, regs, sp), name in zip(recs, names):
+    name = re.sub(r"\(ebisu::TmapSet.*$", "", name).replace("ebisu::", "")
+    print(f"{name:75s} regs={regs:>4s} stack={sp[0]} spill={sp[1]}/{sp[2]}")

@@ -93,14 +93,71 @@ def test_odd_width_and_generic_shapes_use_naive_kernel():
     assert np.array_equal(out.cells, oracle_run(g.cells, taps_of(rev), 7))
 
 
-@pytest.mark.parametrize("name", ["j1d3pt", "j3d7pt", "j3d13pt", "j3d17pt", "j3d27pt",
-                                  "poisson"])
-def test_other_dims_bitwise(name):
-    st = _shape(name)
-    ext = {1: (301,), 3: (17, 19, 24)}[st.dims]
-    g = eb.random_grid(ext, 77)
-    out = eb.reference_run(g, st, 6)
+def test_j1d3pt_naive_bitwise():
+    st = _shape("j1d3pt")
+    g = eb.random_grid((301,), 77)
+    out, tr = eb.sweep(g, st, 6, trace=True)
+    assert tr["kernel"] == "naive_step"
     assert np.array_equal(out.cells, oracle_run(g.cells, taps_of(st), 6))
+
+
+CASES_3D = {
+    "j3d7pt": [1, 2, 3, 4],
+    "j3d13pt": [1, 2],
+    "j3d17pt": [1, 2],
+    "j3d27pt": [1, 2],
+    "poisson": [1, 2],
+}
+
+
+@pytest.mark.parametrize("name", list(CASES_3D))
+def test_3d_shapes_all_depths_ragged(name):
+    st = _shape(name)
+    rng = eb.SplitMix64(hash(name) & 0xFFFF)
+    r = st.radius
+    for t in CASES_3D[name]:
+        for _ in range(3):
+            n0 = 2 * r + 1 + rng.randint(0, 40)
+            n1 = 2 * r + 1 + rng.randint(0, 90)
+            n2 = 2 * (r + 1 + rng.randint(0, 90) // 2)  # even: TMA path
+            steps = rng.randint(1, 2 * t + 2)
+            g = eb.random_grid((n0, n1, n2), rng.next_u64())
+            ref = oracle_run(g.cells, taps_of(st), steps)
+            out, tr = eb.sweep(g, st, steps, t=t, trace=True)
+            assert tr["kernel"] == "stream3d_tb", tr
+            assert np.array_equal(out.cells, ref), (name, t, (n0, n1, n2), steps, tr)
+
+
+def test_3d_lane_variants_and_persistence():
+    st = _shape("j3d7pt")
+    g = eb.random_grid((40, 70, 134), 11)
+    ref = oracle_run(g.cells, taps_of(st), 13)
+    for t in (2, 3, 4):
+        for persistent in (True, False):
+            out = eb.sweep(g, st, 13, t=t, persistent=persistent)
+            assert np.array_equal(out.cells, ref), (t, persistent)
+
+
+def test_3d_odd_last_extent_uses_naive():
+    st = _shape("j3d7pt")
+    g = eb.random_grid((17, 19, 23), 5)
+    out, tr = eb.sweep(g, st, 5, trace=True)
+    assert tr["kernel"] == "naive_step"
+    assert np.array_equal(out.cells, oracle_run(g.cells, taps_of(st), 5))
+
+
+def test_full_size_512_cubed_against_oracle():
+    # BASELINE config 4 geometry (j3d7pt 512^3): one t=3 epoch + 1 remainder step
+    from paper_2305_07390_b200 import device
+
+    torch = _torch()
+    st = eb.make_benchmark("j3d7pt")
+    d_in = device.random_grid_device((512, 512, 512), seed=1)
+    out, tr = device.sweep_device(d_in, st, 4, t=3, trace=True)
+    assert tr["kernel"] == "stream3d_tb"
+    torch.cuda.synchronize()
+    ref = reference_run_threaded(d_in.cpu().numpy(), taps_of(st), 4, os.cpu_count() or 4)
+    assert np.array_equal(out.cpu().numpy(), ref)
 
 
 @pytest.mark.parametrize("name", ["j2d5pt", "j2d25pt", "j3d7pt"])

@@ -1,0 +1,15 @@
+"""Single sweep for ncu captures: python tools/prof_run.py NAME N STEPS T [variant]."""
+import os, sys
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import torch
+import paper_2305_07390_b200 as eb
+from paper_2305_07390_b200 import device, _native
+name, n, steps, t = sys.argv[1], int(sys.argv[2]), int(sys.argv[3]), int(sys.argv[4])
+var = int(sys.argv[5]) if len(sys.argv) > 5 else 0
+st = eb.get_shape(name)
+d_in = device.random_grid_device((n,) * st.dims, seed=1)
+out = torch.empty_like(d_in); scr = torch.empty_like(d_in)
+prm = _native.make_params(t=t, variant=var)
+for _ in range(2):
+    _, tr = device.sweep_device(d_in, st, steps, out=out, scratch=scr, params=prm, trace=True)
+print(tr)
