@@ -191,6 +191,7 @@ def main():
     ap.add_argument("--ref-tsteps", type=int, default=2)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-3d", action="store_true", help="skip the config-4 3-D measurement")
     ap.add_argument("--sweep-t", action="store_true", help="also time t=1..16 (config 2 sweep)")
     args = ap.parse_args()
     if args.warmup < 3:
@@ -352,6 +353,26 @@ def main():
         torch.cuda.synchronize()
         line["naive_gcells"] = round((N0 - 2) * (N1 - 2) * 20 / (a.elapsed_time(b) / 1e3) / 1e9,
                                      1)
+
+    if world == 1 and not args.no_3d:
+        # BASELINE config 4 (j3d7pt fp64 512^3, 500 steps), same exact mode
+        st3 = eb.make_benchmark("j3d7pt")
+        d3 = device.random_grid_device((512, 512, 512), seed=1)
+        o3 = torch.empty_like(d3)
+        s3 = torch.empty_like(d3)
+        device.sweep_device(d3, st3, 500, out=o3, scratch=s3)
+        torch.cuda.synchronize()
+        times = []
+        for _ in range(2):
+            _, tr3 = device.sweep_device(d3, st3, 500, out=o3, scratch=s3, trace=True)
+            times.append(tr3["elapsed_ms"])
+        ms3 = min(times)
+        line["config4_j3d7pt_512"] = {
+            "metric": "GCells/s (fp64)", "value": 510 ** 3 * 500 / (ms3 / 1e3) / 1e9,
+            "ms_per_sweep": ms3, "time_steps": 500, "fused_depth_t": tr3["t_used"],
+            "kernel": tr3["kernel"], "exact": True,
+            "naive_roofline_frac": 16 * 510 ** 3 * 500 / (ms3 / 1e3) / 1e9 / hbm_peak}
+        del d3, o3, s3
 
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         line["cpu_baseline"] = cpu_oracle_sample()
