@@ -218,10 +218,11 @@ def main():
     if world > 1:
         from paper_2305_07390_b200 import distributed as edist
 
-        runner = edist.SlabSweep(st, (N0, N1), t=args.t, seed=1, exact=True)
+        # weak scaling: every rank owns an N0 x N1 slab of a (world*N0) x N1 grid
+        runner = edist.SlabSweep(st, (N0 * world, N1), t=args.t, seed=1, exact=True)
         step = lambda: runner.run(args.tsteps)  # noqa: E731
         cells_per_step = runner.global_interior_cells() * args.tsteps
-        launches_per_step = None
+        launches_per_step = -(-args.tsteps // args.t)  # one epoch launch per exchange
     else:
         d_in = device.random_grid_device((N0, N1), seed=1)
         d_out = torch.empty_like(d_in)
@@ -266,16 +267,16 @@ def main():
         dist.all_reduce(ms_t, op=dist.ReduceOp.MAX)
     ms = float(ms_t.item())
     step_ms = [a.elapsed_time(b) for a, b in per_launch]
-    value = cells_per_step * world * args.steps / (ms / 1e3) / 1e9
+    value = cells_per_step * args.steps / (ms / 1e3) / 1e9  # whole job (all ranks)
 
     hbm_peak, peak_kind = _peaks()
     # dominant kernel: one stream2d_tb launch per bench step when tsteps % t == 0
     # (persistent cooperative launch, grid.sync between epochs)
     launch_ms = statistics.mean(step_ms)
-    achieved = ALG_BYTES_PER_CELL_STEP * cells_per_step / (launch_ms / 1e3) / 1e9
+    achieved = ALG_BYTES_PER_CELL_STEP * cells_per_step / world / (launch_ms / 1e3) / 1e9
     traffic = None
     tf = os.path.join(ROOT, "profiles", "dram_traffic.json")
-    if os.path.exists(tf):
+    if os.path.exists(tf) and args.tsteps == TSTEPS and world == 1:
         try:
             traffic = json.load(open(tf)).get(f"{STENCIL}_t{args.t}")
         except Exception:

@@ -1,0 +1,221 @@
+"""Multi-GPU sweep: slab decomposition along axis 0.
+
+Not in the reference (it has no distributed backend); this is the
+B200 build's scale-out of ``reference_run`` over the GPUs of one node.
+
+* Rank g owns the contiguous planes ``[own0, own1)`` of axis 0 (the streaming
+  axis, slowest in C order, so slabs and halos are contiguous blocks).
+* Each rank keeps ``H = t*R`` ghost planes on every interior face.  Per epoch
+  (t fused steps): exchange H boundary planes with each neighbour (NCCL
+  point-to-point ``send/recv`` through ``torch.distributed``, one batched group
+  per epoch), then run the epoch on ghost+owned planes with the single-GPU
+  kernel (``ebisu_run_device``).  The array faces at ghost boundaries are
+  treated as frame by the kernel; the error this introduces travels R planes
+  per step, so after t steps it has crossed exactly the H ghost planes and the
+  owned planes are exact -- bitwise equal to ``reference_run`` on the full
+  grid (tests/test_distributed.py).
+* Global frame planes belong to the first/last rank, which have no ghost on
+  that face, so the kernel's own frame handling applies there.
+
+The compute step is a parameter only so that the CPU tests can drive the same
+exchange logic with the oracle; the product default is the GPU kernel.
+"""
+
+from __future__ import annotations
+
+from dataclasses import dataclass
+
+from .shapes import StencilShape
+
+
+@dataclass(frozen=True)
+class SlabPlan:
+    """One rank's share of axis 0 (all indices are global plane numbers)."""
+
+    rank: int
+    world: int
+    n0: int
+    own0: int
+    own1: int
+    ghost_lo: int  # ghost planes below own0 held locally
+    ghost_hi: int  # ghost planes above own1 held locally
+
+    @property
+    def local0(self) -> int:
+        return self.own0 - self.ghost_lo
+
+    @property
+    def local1(self) -> int:
+        return self.own1 + self.ghost_hi
+
+    @property
+    def local_planes(self) -> int:
+        return self.local1 - self.local0
+
+
+def slab_plan(n0: int, world: int, rank: int, halo: int) -> SlabPlan:
+    """Even split of ``n0`` planes; ``halo`` ghost planes per interior face."""
+    if world < 1 or not 0 <= rank < world:
+        raise ValueError("bad rank/world")
+    base, extra = divmod(n0, world)
+    own0 = rank * base + min(rank, extra)
+    own1 = own0 + base + (1 if rank < extra else 0)
+    if world > 1 and base < halo:
+        raise ValueError(
+            f"slab of {base} planes is thinner than the {halo}-plane halo; "
+            "use fewer ranks or a smaller fused depth"
+        )
+    lo = halo if rank > 0 else 0
+    hi = halo if rank < world - 1 else 0
+    return SlabPlan(rank, world, n0, own0, own1, lo, hi)
+
+
+def _default_step(stencil: StencilShape, exact: bool):
+    from . import device
+
+    def step(src, dst, scratch, steps, t):
+        device.sweep_device(src, stencil, steps, out=dst, scratch=scratch, t=t, exact=exact)
+
+    return step
+
+
+class SlabSweep:
+    """Distributed ``reference_run`` over ``torch.distributed`` ranks.
+
+    ``extents`` is the GLOBAL grid shape; each rank allocates only its slab
+    plus ghosts.  ``seed`` draws the global SplitMix64 grid, each rank
+    generating exactly its own planes (``ebisu_random_grid_device`` with the
+    global start offset).
+    """
+
+    def __init__(self, stencil: StencilShape, extents, t: int, seed: int | None = None,
+                 exact: bool = True, group=None, device=None, step=None, cells=None):
+        import torch
+        import torch.distributed as dist
+
+        self.torch, self.dist = torch, dist
+        self.stencil = stencil
+        self.extents = tuple(int(n) for n in extents)
+        self.t = int(t)
+        self.group = group
+        self.rank = dist.get_rank(group) if dist.is_initialized() else 0
+        self.world = dist.get_world_size(group) if dist.is_initialized() else 1
+        self.halo = self.t * stencil.radius
+        self.plan = slab_plan(self.extents[0], self.world, self.rank, self.halo)
+        self.device = device if device is not None else (
+            torch.device("cuda", torch.cuda.current_device()) if torch.cuda.is_available()
+            else torch.device("cpu"))
+        self.step = step if step is not None else _default_step(stencil, exact)
+        rest = self.extents[1:]
+        shape = (self.plan.local_planes,) + rest
+        plane = 1
+        for n in rest:
+            plane *= n
+        self.plane_cells = plane
+        if cells is not None:
+            a = cells.to(self.device, dtype=torch.float64).contiguous()
+            if tuple(a.shape) != shape:
+                raise ValueError(f"local slab must have shape {shape}")
+        else:
+            a = torch.empty(shape, dtype=torch.float64, device=self.device)
+            if seed is not None:
+                self._fill_random(a, seed)
+        self.a = a
+        self.b = torch.empty_like(a)
+        self.scratch = torch.empty_like(a)
+
+    # -- data --------------------------------------------------------------
+    def _fill_random(self, a, seed: int):
+        if a.is_cuda:
+            import ctypes  # noqa: F401
+
+            from . import _native, device
+
+            lib = _native.load()
+            rc = lib.ebisu_random_grid_device(int(seed) & ((1 << 64) - 1),
+                                              self.plan.local0 * self.plane_cells, a.numel(),
+                                              a.data_ptr(), device._stream_ptr())
+            if rc:
+                raise _native.NativeError(_native.last_error())
+        else:
+            from .rng import uniform_array
+
+            vals = uniform_array(seed, a.numel(), start=self.plan.local0 * self.plane_cells)
+            a.copy_(self.torch.from_numpy(vals.reshape(tuple(a.shape))))
+
+    def owned(self):
+        """This rank's owned planes of the current state (a view)."""
+        p = self.plan
+        return self.a[p.ghost_lo:p.ghost_lo + (p.own1 - p.own0)]
+
+    def global_interior_cells(self) -> int:
+        r = self.stencil.radius
+        n = 1
+        for e in self.extents:
+            n *= e - 2 * r
+        return n
+
+    # -- communication ---------------------------------------------------------
+    def exchange(self, depth: int):
+        """Refresh ``depth`` ghost planes on each interior face."""
+        if self.world == 1 or depth == 0:
+            return
+        dist = self.dist
+        p = self.plan
+        a = self.a
+        own_n = p.own1 - p.own0
+        ops = []
+        recv_lo = recv_hi = None
+        if p.rank > 0:
+            send_lo = a[p.ghost_lo:p.ghost_lo + depth].contiguous()
+            recv_lo = self.torch.empty_like(send_lo)
+            ops.append(dist.P2POp(dist.isend, send_lo, p.rank - 1, self.group))
+            ops.append(dist.P2POp(dist.irecv, recv_lo, p.rank - 1, self.group))
+        if p.rank < p.world - 1:
+            hi0 = p.ghost_lo + own_n
+            send_hi = a[hi0 - depth:hi0].contiguous()
+            recv_hi = self.torch.empty_like(send_hi)
+            ops.append(dist.P2POp(dist.isend, send_hi, p.rank + 1, self.group))
+            ops.append(dist.P2POp(dist.irecv, recv_hi, p.rank + 1, self.group))
+        for w in dist.batch_isend_irecv(ops):
+            w.wait()
+        if recv_lo is not None:
+            a[p.ghost_lo - depth:p.ghost_lo].copy_(recv_lo)
+        if recv_hi is not None:
+            hi0 = p.ghost_lo + own_n
+            a[hi0:hi0 + depth].copy_(recv_hi)
+
+    # -- sweep ------------------------------------------------------------------
+    def run(self, steps: int):
+        """Advance the distributed grid by ``steps`` Jacobi steps."""
+        if steps < 0:
+            raise ValueError("step count must be >= 0")
+        done = 0
+        while done < steps:
+            d = min(self.t, steps - done)
+            self.exchange(d * self.stencil.radius)
+            self.step(self.a, self.b, self.scratch, d, d)
+            self.a, self.b = self.b, self.a
+            done += d
+        return self.owned()
+
+    def gather(self, dst: int = 0):
+        """Full grid on rank ``dst`` (tests / verification); None elsewhere."""
+        torch, dist = self.torch, self.dist
+        own = self.owned().contiguous()
+        if self.world == 1:
+            return own.cpu()
+        sizes = [slab_plan(self.extents[0], self.world, r, self.halo) for r in range(self.world)]
+        if self.rank == dst:
+            parts = []
+            for r, pr in enumerate(sizes):
+                if r == dst:
+                    parts.append(own.cpu())
+                else:
+                    buf = torch.empty((pr.own1 - pr.own0,) + self.extents[1:],
+                                      dtype=torch.float64, device=own.device)
+                    dist.recv(buf, src=r, group=self.group)
+                    parts.append(buf.cpu())
+            return torch.cat(parts, 0)
+        dist.send(own, dst=dst, group=self.group)
+        return None
