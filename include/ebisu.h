@@ -92,8 +92,15 @@ typedef struct ebisu_params {
   int32_t lane_cells;        /* cells per lane along the fastest axis (0 = planner) */
   int32_t seg_rows;          /* rows per work unit along axis 0 (0 = planner)       */
   int32_t variant;           /* n-th registered kernel for (shape, t) (0 = default) */
-  int32_t reserved[3];
+  int32_t per_tap_products;  /* 1: never share products between taps (see below)   */
+  int32_t reserved[2];
 } ebisu_params;
+/* Shared products: when every coefficient of the stencil is bitwise equal (the
+ * catalog default 1/|taps|, shapes.py:148-157), term_k = RN(c*x_k) depends on
+ * the cell only, so the kernels compute it once per cell and level and every
+ * tap reuses it.  The sums keep the reference order, so the result is still
+ * bitwise equal to reference_run; only the DMUL count drops (13 -> 7 DP ops
+ * per j3d7pt cell-step).  per_tap_products=1 forces the per-tap kernels. */
 
 /* Closed-form execution counters of the GPU run (reference ExecutionTrace,
  * engine/trace.py:25-40), plus GPU facts. */

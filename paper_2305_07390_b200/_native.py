@@ -74,7 +74,8 @@ class ParamsC(ctypes.Structure):
         ("lane_cells", ctypes.c_int32),
         ("seg_rows", ctypes.c_int32),
         ("variant", ctypes.c_int32),
-        ("reserved", ctypes.c_int32 * 3),
+        ("per_tap_products", ctypes.c_int32),
+        ("reserved", ctypes.c_int32 * 2),
     ]
 
 
@@ -191,7 +192,8 @@ class StencilArgs:
 def make_params(scheme: int = SCHEME_AUTO, t: int = 0, tile=(0, 0), device_tile_grid=(0, 0),
                 lazy: bool = False, exact: bool = True, persistent: bool = True,
                 validate_tile: bool = False, lane_cells: int = 0,
-                seg_rows: int = 0, variant: int = 0) -> ParamsC:
+                seg_rows: int = 0, variant: int = 0,
+                per_tap_products: bool = False) -> ParamsC:
     p = ParamsC()
     p.scheme = scheme
     p.t = int(t)
@@ -206,6 +208,7 @@ def make_params(scheme: int = SCHEME_AUTO, t: int = 0, tile=(0, 0), device_tile_
     p.lane_cells = int(lane_cells)
     p.seg_rows = int(seg_rows)
     p.variant = int(variant)
+    p.per_tap_products = int(bool(per_tap_products))
     return p
 
 

@@ -240,26 +240,41 @@ enum KernelId : int {
 
 // First registered kernel for (shape, depth, exactness) -- the registry lists
 // the planner's default lane width first -- or the one with lane width C.
-const TbKernel* find_tb(int shape_id, int dims, int T, bool exact, int C = 0, int variant = 0) {
+// Kernel family for a request: shared-product kernels (uni) are bitwise exact,
+// so they serve both exact and FMA requests when the coefficients are uniform.
+bool family_ok(const TbKernel& k, bool exact, bool uni) {
+  if (uni) return k.uni != 0;
+  return k.uni == 0 && (k.exact != 0) == exact;
+}
+
+const TbKernel* find_tb(int shape_id, int dims, int T, bool exact, bool uni, int C = 0,
+                        int variant = 0) {
   int n = 0;
   const TbKernel* ks = tb_kernels(&n);
   for (int i = 0; i < n; ++i)
     if (ks[i].shape_id == shape_id && ks[i].dims == dims && ks[i].T == T &&
-        (ks[i].exact != 0) == exact && (C == 0 || ks[i].C == C)) {
+        family_ok(ks[i], exact, uni) && (C == 0 || ks[i].C == C)) {
       if (variant-- == 0) return &ks[i];
     }
   return nullptr;
 }
 
 // largest instantiated depth <= tmax for this shape
-int best_depth_leq(int shape_id, int dims, int tmax, bool exact) {
+int best_depth_leq(int shape_id, int dims, int tmax, bool exact, bool uni) {
   int n = 0, best = 0;
   const TbKernel* ks = tb_kernels(&n);
   for (int i = 0; i < n; ++i)
-    if (ks[i].shape_id == shape_id && ks[i].dims == dims && (ks[i].exact != 0) == exact &&
+    if (ks[i].shape_id == shape_id && ks[i].dims == dims && family_ok(ks[i], exact, uni) &&
         ks[i].T <= tmax)
       best = std::max(best, ks[i].T);
   return best;
+}
+
+// Every coefficient bitwise equal (the catalog default, shapes.py:156-157)?
+bool uniform_coeffs(const ProblemDesc& p) {
+  for (int i = 1; i < p.ntaps; ++i)
+    if (memcmp(&p.coeffs[i], &p.coeffs[0], sizeof(double)) != 0) return false;
+  return true;
 }
 
 // Default fused depth (measured sweet spot on B200).
@@ -533,6 +548,7 @@ int run_device_impl(const ProblemDesc& p, const double* d_in, double* d_out, dou
   // ---- plan the stage list ----------------------------------------------------
   std::vector<Stage> stages;
   const int D = p.dims;
+  const bool uni = uniform_coeffs(p) && !(prm && prm->per_tap_products);
   // TMA needs 16-byte row strides (even last extent) and 16-byte aligned bases.
   bool tb_ok = (D == 2 || D == 3) && p.shape_id != SHAPE_GENERIC &&
                scheme != EBISU_SCHEME_NAIVE && (p.ext[D - 1] % 2 == 0) &&
@@ -543,15 +559,15 @@ int run_device_impl(const ProblemDesc& p, const double* d_in, double* d_out, dou
     int t = (prm && prm->t > 0) ? prm->t : default_depth(p.shape_id);
     const int want_c = prm ? prm->lane_cells : 0;
     const int want_v = prm ? prm->variant : 0;
-    const TbKernel* k = find_tb(p.shape_id, D, t, exact, want_c, want_v);
+    const TbKernel* k = find_tb(p.shape_id, D, t, exact, uni, want_c, want_v);
     if (!k && (want_c || want_v))
       return fail(EBISU_ERR_UNSUPPORTED, "no kernel with depth %d, %d cells per lane, variant %d",
                   t, want_c, want_v);
     if (!k) {
       // depth not instantiated: compose the sweep from the deepest kernel
       // below it (epochs compose bitwise, test_grid.py:94-117)
-      t = best_depth_leq(p.shape_id, D, t, exact);
-      k = t ? find_tb(p.shape_id, D, t, exact) : nullptr;
+      t = best_depth_leq(p.shape_id, D, t, exact, uni);
+      k = t ? find_tb(p.shape_id, D, t, exact, uni) : nullptr;
     }
     if (!k) {
       tb_ok = false;
@@ -561,13 +577,13 @@ int run_device_impl(const ProblemDesc& p, const double* d_in, double* d_out, dou
       const int kid = D == 2 ? KID_STREAM2D : KID_STREAM3D;
       if (full > 0) stages.push_back({kid, k, (int)full});
       while (rem > 0) {
-        const int t2 = best_depth_leq(p.shape_id, D, (int)rem, exact);
+        const int t2 = best_depth_leq(p.shape_id, D, (int)rem, exact, uni);
         if (t2 == 0) {
           stages.push_back({KID_NAIVE, nullptr, (int)rem});
           break;
         }
         const long long e2 = rem / t2;
-        stages.push_back({kid, find_tb(p.shape_id, D, t2, exact), (int)e2});
+        stages.push_back({kid, find_tb(p.shape_id, D, t2, exact, uni), (int)e2});
         rem -= e2 * t2;
       }
     }
@@ -588,6 +604,22 @@ int run_device_impl(const ProblemDesc& p, const double* d_in, double* d_out, dou
   }
   double* bufs[3] = {const_cast<double*>(d_in), d_out, scr};
   CUtensorMap maps[3];
+  // Shared-product kernels never store frame cells (their windows hold
+  // products, not values); the frame is constant, so copy it once into both
+  // ping-pong buffers (a shell of 2R planes/rows/columns, not the grid).
+  bool any_uni = false;
+  for (auto& s : stages) any_uni = any_uni || (s.k && s.k->uni);
+  if (any_uni) {
+    for (int b = BUF_OUT; b <= BUF_SCR; ++b) {
+      if (!bufs[b]) continue;
+      cudaError_t e = launch_frame_copy(p, d_in, bufs[b], st, di.sms);
+      if (e != cudaSuccess) {
+        if (own_scr) cudaFreeAsync(scr, st);
+        return cuda_fail(e, "frame copy launch");
+      }
+      ctr->launches += 1;
+    }
+  }
 
   // write w (0-based) goes to OUT iff (nwrites-1-w) is even
   long long w = 0;

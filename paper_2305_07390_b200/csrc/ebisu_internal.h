@@ -30,6 +30,8 @@ struct ProblemDesc {
 
 cudaError_t launch_naive_step(const ProblemDesc& p, const double* in, double* out, bool exact,
                               cudaStream_t st, int num_sms);
+cudaError_t launch_frame_copy(const ProblemDesc& p, const double* in, double* out,
+                              cudaStream_t st, int num_sms);
 cudaError_t launch_splitmix(unsigned long long seed, long long start, long long n, double* out,
                             cudaStream_t st, int num_sms);
 cudaError_t launch_compare(const double* a, const double* b, long long n, long long* mism,
@@ -63,6 +65,7 @@ struct TbKernel {
   int NW;        // warps per CTA
   int S;         // ring slots
   int exact;
+  int uni;       // shared-product kernel (uniform coefficients; bitwise exact)
   int smem_bytes;
   int box0, box1, box2;  // TMA box (elements) fastest first
   int valid_x;           // valid columns per warp strip (2-D) or per tile (3-D, axis 2)

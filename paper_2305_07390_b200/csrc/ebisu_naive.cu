@@ -77,6 +77,55 @@ cudaError_t launch_naive_step(const ProblemDesc& p, const double* in, double* ou
   return cudaGetLastError();
 }
 
+// ---- frame pre-copy -----------------------------------------------------------
+// Copies the Dirichlet frame (cells within R of any face, common.py:96-112)
+// from `in` to `out`.  One warp per row of the fastest axis: frame rows are
+// copied whole, other rows only their first and last R cells.
+__global__ void __launch_bounds__(256) k_frame_copy(const double* __restrict__ in,
+                                                    double* __restrict__ out, long long P,
+                                                    long long Y, long long X, int R0, int R1,
+                                                    int R2) {
+  const int lane = threadIdx.x & 31;
+  const long long warps = (long long)gridDim.x * (blockDim.x >> 5);
+  for (long long row = (long long)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+       row < P * Y; row += warps) {
+    const long long pp = row / Y, y = row % Y;
+    const double* src = in + row * X;
+    double* dst = out + row * X;
+    if (pp < R0 || pp >= P - R0 || y < R1 || y >= Y - R1) {
+      for (long long j = lane; j < X; j += 32) dst[j] = src[j];
+    } else {
+      for (int j = lane; j < 2 * R2; j += 32) {
+        const long long x = j < R2 ? j : X - 2 * R2 + j;
+        dst[x] = src[x];
+      }
+    }
+  }
+}
+
+cudaError_t launch_frame_copy(const ProblemDesc& p, const double* in, double* out,
+                              cudaStream_t st, int num_sms) {
+  long long P = 1, Y = 1, X = p.ext[0];
+  int R0 = 0, R1 = 0;
+  if (p.dims == 2) {
+    Y = p.ext[0];
+    X = p.ext[1];
+    R1 = p.rad;
+  } else if (p.dims == 3) {
+    P = p.ext[0];
+    Y = p.ext[1];
+    X = p.ext[2];
+    R0 = R1 = p.rad;
+  }
+  const long long rows = P * Y;
+  long long blocks = (rows + 7) / 8;
+  const long long cap = (long long)num_sms * 8;
+  if (blocks > cap) blocks = cap;
+  if (blocks < 1) blocks = 1;
+  k_frame_copy<<<(unsigned)blocks, 256, 0, st>>>(in, out, P, Y, X, R0, R1, p.rad);
+  return cudaGetLastError();
+}
+
 // ---- SplitMix64 uniforms, bit-identical to rng.uniform_array ---------------
 __global__ void __launch_bounds__(256) k_splitmix_uniform(unsigned long long seed,
                                                           long long start, long long n,

@@ -139,7 +139,7 @@ __host__ __device__ constexpr int pmod(int a) {
 
 // One work unit (warp strip x row segment) of one epoch.  FC selects the
 // frame-column handling (see StripGeom); frame rows are handled per block.
-template <class SH, int T, int C, int S, bool EXACT, int FC>
+template <class SH, int T, int C, int S, bool EXACT, bool UNI, int FC>
 __device__ __forceinline__ void stream2d_unit(const CUtensorMap* tm, double* __restrict__ out,
                                               double* ring, uint64_t* bars, uint32_t ring_cnt,
                                               int lane, int n0, int n1, const StripGeom& g,
@@ -233,8 +233,9 @@ __device__ __forceinline__ void stream2d_unit(const CUtensorMap* tm, double* __r
 #pragma unroll
           for (int c = 0; c < C; ++c) v[c] = 0.0;
         }
+        // UNI: the window holds products y = c*x (one DMUL per cell per level)
 #pragma unroll
-        for (int c = 0; c < C; ++c) win[0][uu][c] = v[c];
+        for (int c = 0; c < C; ++c) win[0][uu][c] = UNI ? __dmul_rn(cf.c[0], v[c]) : v[c];
       }
       // ---- levels 1..T ----------------------------------------------------
       // Every level runs every advance.  During pipeline warm-up a level's
@@ -280,27 +281,33 @@ __device__ __forceinline__ void stream2d_unit(const CUtensorMap* tm, double* __r
               x = hr[o.d0 + R][cc - C];
             else
               x = win[s - 1][sl][cc];
-            if constexpr (i == 0)
+            if constexpr (UNI)
+              acc[c] = (i == 0) ? x : __dadd_rn(acc[c], x);
+            else if constexpr (i == 0)
               acc[c] = tap_first<EXACT>(cf.c[0], x);
             else
               acc[c] = tap_next<EXACT>(acc[c], cf.c[i], x);
           }
         });
-        // frame cells carry level s-1's centre (branch-free selects)
+        // frame cells carry level s-1's centre (branch-free selects); in UNI
+        // mode the carried centre is the product c*x, which is the frame's
+        // product at every level, and level T never stores frame cells (the
+        // host pre-copies the frame into both ping-pong buffers)
         double nv[C];
         bool frow = false;
         if constexpr (FROWS) frow = (q < R) || (q >= n0 - R);
 #pragma unroll
         for (int c = 0; c < C; ++c) {
           const double centre = win[s - 1][pmod<W>(uu - s * R)][c];
+          const double val = (UNI && s < T) ? __dmul_rn(cf.c[0], acc[c]) : acc[c];
           if (FROWS && col_may_frame(c))
-            nv[c] = (frow || fcol[c]) ? centre : acc[c];
+            nv[c] = (frow || fcol[c]) ? centre : val;
           else if (FROWS)
-            nv[c] = frow ? centre : acc[c];
+            nv[c] = frow ? centre : val;
           else if (col_may_frame(c))
-            nv[c] = fcol[c] ? centre : acc[c];
+            nv[c] = fcol[c] ? centre : val;
           else
-            nv[c] = acc[c];
+            nv[c] = val;
         }
         if constexpr (s < T) {
 #pragma unroll
@@ -309,8 +316,14 @@ __device__ __forceinline__ void stream2d_unit(const CUtensorMap* tm, double* __r
           if (q >= r0 && q < r1) {
             double* orow = out + (size_t)q * (size_t)n1 + (X0 + lane * C);
 #pragma unroll
-            for (int c = 0; c < C; ++c)
-              if (stcol[c]) orow[c] = nv[c];
+            for (int c = 0; c < C; ++c) {
+              bool st = stcol[c];
+              if constexpr (UNI) {
+                if (FROWS) st = st && !frow;
+                if (col_may_frame(c)) st = st && !fcol[c];
+              }
+              if (st) orow[c] = nv[c];
+            }
           }
         }
       });
@@ -334,7 +347,7 @@ __device__ __forceinline__ int next_unit(int* counter, int lane) {
   return __shfl_sync(kFullMask, u, 0);
 }
 
-template <class SH, int T, int C, int NW, int S, bool EXACT, int MINB>
+template <class SH, int T, int C, int NW, int S, bool EXACT, bool UNI, int MINB>
 __global__ void __launch_bounds__(NW * 32, MINB)
     k_stream2d(const __grid_constant__ TmapSet maps, const Stream2DArgs a,
                const __grid_constant__ Coefs<SH::NT> cf) {
@@ -383,23 +396,23 @@ __global__ void __launch_bounds__(NW * 32, MINB)
       if (a.unit_clock && e == 0 && lane == 0)
         asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_start));
       if constexpr (R > C) {
-        stream2d_unit<SH, T, C, S, EXACT, 3>(tm, out, ring, bars, ring_cnt, lane, n0, n1, g, r0,
+        stream2d_unit<SH, T, C, S, EXACT, UNI, 3>(tm, out, ring, bars, ring_cnt, lane, n0, n1, g, r0,
                                              r1, cf);
       } else switch (g.fc) {
         case 0:
-          stream2d_unit<SH, T, C, S, EXACT, 0>(tm, out, ring, bars, ring_cnt, lane, n0, n1, g,
+          stream2d_unit<SH, T, C, S, EXACT, UNI, 0>(tm, out, ring, bars, ring_cnt, lane, n0, n1, g,
                                                r0, r1, cf);
           break;
         case 1:
-          stream2d_unit<SH, T, C, S, EXACT, 1>(tm, out, ring, bars, ring_cnt, lane, n0, n1, g,
+          stream2d_unit<SH, T, C, S, EXACT, UNI, 1>(tm, out, ring, bars, ring_cnt, lane, n0, n1, g,
                                                r0, r1, cf);
           break;
         case 2:
-          stream2d_unit<SH, T, C, S, EXACT, 2>(tm, out, ring, bars, ring_cnt, lane, n0, n1, g,
+          stream2d_unit<SH, T, C, S, EXACT, UNI, 2>(tm, out, ring, bars, ring_cnt, lane, n0, n1, g,
                                                r0, r1, cf);
           break;
         default:
-          stream2d_unit<SH, T, C, S, EXACT, 3>(tm, out, ring, bars, ring_cnt, lane, n0, n1, g,
+          stream2d_unit<SH, T, C, S, EXACT, UNI, 3>(tm, out, ring, bars, ring_cnt, lane, n0, n1, g,
                                                r0, r1, cf);
           break;
       }

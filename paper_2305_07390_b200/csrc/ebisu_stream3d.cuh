@@ -73,10 +73,10 @@ __host__ __device__ constexpr bool row_needs_x_halo(int dz, int ey, int CY) {
   return false;
 }
 
-template <class SH, int T, int CY, int CX, int NWY, int S, bool DEC = false>
+template <class SH, int T, int CY, int CX, int NWY, int S, int FL = 0>
 struct Stream3DCfg {
   static constexpr int R = SH::R;
-  static constexpr int Z = (offcentre_inplane<SH>() || DEC) ? R + 1 : R;  // level skew
+  static constexpr int Z = (offcentre_inplane<SH>() || (FL & 1)) ? R + 1 : R;  // level skew
   static constexpr int WN = 2 * R + (Z - R) + 1;                   // window planes
   static constexpr int NB = offcentre_inplane<SH>() ? Z + R + 1 : Z + 1;  // halo buffers
   static constexpr int LY = NWY * CY;
@@ -92,7 +92,11 @@ struct Stream3DCfg {
   static constexpr int RING_PLANE = LY * LX;          // doubles per ring slot
   static constexpr int RING_BYTES = S * RING_PLANE * 8;
   static constexpr int HALO_BYTES = T * NB * HPLANE * 8;
-  static constexpr int SMEM_BYTES = RING_BYTES + HALO_BYTES + S * 8;
+  static constexpr int SMEM_BYTES = RING_BYTES + HALO_BYTES + (S + 1) * 8;
+  // FL bit 1 (SPLIT): the per-advance __syncthreads becomes a split-phase
+  // mbarrier (every thread arrives after its pushes; pulls of advance k wait
+  // for phase k-1), so warps drift by up to one advance instead of draining.
+  static constexpr bool SPLIT = (FL & 2) != 0;
   static_assert(CY >= R, "a warp's rows must cover the radius");
   static_assert(VY > 0 && VX > 0, "tile leaves no valid core");
   static_assert(LX <= 256 && LY <= 256, "TMA box dims are limited to 256");
@@ -100,13 +104,14 @@ struct Stream3DCfg {
   static_assert(SMEM_BYTES <= 227 * 1024, "shared memory budget");
 };
 
-template <class SH, int T, int CY, int CX, int NWY, int S, bool DEC, bool EXACT, bool EDGE>
+template <class SH, int T, int CY, int CX, int NWY, int S, int FL, bool EXACT, bool UNI, bool EDGE>
 __device__ __forceinline__ void stream3d_unit(const CUtensorMap* tm, double* __restrict__ out,
                                               double* ring, double* halo, uint64_t* bars,
-                                              uint32_t ring_cnt, int warp, int lane, int n0,
+                                              uint32_t ring_cnt, uint32_t& adv, int warp,
+                                              int lane, int n0,
                                               int n1, int n2, int X0, int Y0, int r0, int r1,
                                               const Coefs<SH::NT>& cf) {
-  using Cfg = Stream3DCfg<SH, T, CY, CX, NWY, S, DEC>;
+  using Cfg = Stream3DCfg<SH, T, CY, CX, NWY, S, FL>;
   constexpr int R = Cfg::R, Z = Cfg::Z, WN = Cfg::WN, NB = Cfg::NB;
   constexpr int LY = Cfg::LY, LX = Cfg::LX, HY = Cfg::HY, HX = Cfg::HX;
   constexpr int PLANE_BYTES = LY * LX * 8;
@@ -180,6 +185,17 @@ __device__ __forceinline__ void stream3d_unit(const CUtensorMap* tm, double* __r
     for (int uu = 0; uu < WN; ++uu) {
       const int k = kbase + uu;
       const int bk = k % NB;  // halo buffer written this advance
+      if constexpr (Cfg::SPLIT) {
+        // all pushes of the previous advance visible; all its ring reads done
+        if (adv > 0) mbar_wait(&bars[S], (adv - 1) & 1);
+        const int kp = k - 1;
+        if (tid == 0 && kp >= ka && kp < kb && kp + S < kb) {
+          const uint32_t pos = ring_cnt + (uint32_t)(kp - ka);
+          const uint32_t slot = pos & (S - 1);
+          mbar_arrive_expect_tx(&bars[slot], PLANE_BYTES);
+          tma_load_3d(ring + slot * Cfg::RING_PLANE, tm, X0, Y0, kp + S, &bars[slot]);
+        }
+      }
       // ---- level 0 ----------------------------------------------------------
       {
         double v[CY][CX];
@@ -207,6 +223,13 @@ __device__ __forceinline__ void stream3d_unit(const CUtensorMap* tm, double* __r
           for (int cy = 0; cy < CY; ++cy)
 #pragma unroll
             for (int cx = 0; cx < CX; ++cx) v[cy][cx] = 0.0;
+        }
+        // UNI: windows and halos carry products y = c*x (one DMUL per cell)
+        if constexpr (UNI) {
+#pragma unroll
+          for (int cy = 0; cy < CY; ++cy)
+#pragma unroll
+            for (int cx = 0; cx < CX; ++cx) v[cy][cx] = __dmul_rn(cf.c[0], v[cy][cx]);
         }
 #pragma unroll
         for (int cy = 0; cy < CY; ++cy)
@@ -291,7 +314,9 @@ __device__ __forceinline__ void stream3d_unit(const CUtensorMap* tm, double* __r
                   x = ext[o.d0 + R][cy + o.d1 + R][cx + o.d2 + R];
                 else
                   x = win[s - 1][pmod<WN>(uu - s * Z + o.d0)][cy][cx];
-                if constexpr (i == 0)
+                if constexpr (UNI)
+                  acc[cy][cx] = (i == 0) ? x : __dadd_rn(acc[cy][cx], x);
+                else if constexpr (i == 0)
                   acc[cy][cx] = tap_first<EXACT>(cf.c[0], x);
                 else
                   acc[cy][cx] = tap_next<EXACT>(acc[cy][cx], cf.c[i], x);
@@ -302,12 +327,16 @@ __device__ __forceinline__ void stream3d_unit(const CUtensorMap* tm, double* __r
           for (int cy = 0; cy < CY; ++cy)
 #pragma unroll
             for (int cx = 0; cx < CX; ++cx) {
+              // UNI: levels < T carry products; a frame cell's product never
+              // changes, and level T skips frame cells (host pre-copies them)
+              const double val =
+                  (UNI && s < T) ? __dmul_rn(cf.c[0], acc[cy][cx]) : acc[cy][cx];
               if constexpr (EDGE)
                 nv[cy][cx] = (frame_plane || fcell[cy][cx])
                                  ? win[s - 1][pmod<WN>(uu - s * Z)][cy][cx]
-                                 : acc[cy][cx];
+                                 : val;
               else
-                nv[cy][cx] = acc[cy][cx];
+                nv[cy][cx] = val;
             }
         }
         if constexpr (s < T) {
@@ -324,27 +353,33 @@ __device__ __forceinline__ void stream3d_unit(const CUtensorMap* tm, double* __r
             for (int cy = 0; cy < CY; ++cy)
 #pragma unroll
               for (int cx = 0; cx < CX; ++cx)
-                if (stcell[cy][cx]) out[base + (long long)cy * n2 + cx] = nv[cy][cx];
+                if (stcell[cy][cx] && !(UNI && EDGE && (frame_plane || fcell[cy][cx])))
+                  out[base + (long long)cy * n2 + cx] = nv[cy][cx];
           }
         }
       });
-      // one barrier per advance: halo pushes visible, ring slot k consumed
-      __syncthreads();
-      if (tid == 0 && k < kb && k + S < kb) {
-        const uint32_t pos = ring_cnt + (uint32_t)(k - ka);
-        const uint32_t slot = pos & (S - 1);
-        mbar_arrive_expect_tx(&bars[slot], PLANE_BYTES);
-        tma_load_3d(ring + slot * Cfg::RING_PLANE, tm, X0, Y0, k + S, &bars[slot]);
+      if constexpr (Cfg::SPLIT) {
+        mbar_arrive(&bars[S]);
+        ++adv;
+      } else {
+        // one barrier per advance: halo pushes visible, ring slot k consumed
+        __syncthreads();
+        if (tid == 0 && k < kb && k + S < kb) {
+          const uint32_t pos = ring_cnt + (uint32_t)(k - ka);
+          const uint32_t slot = pos & (S - 1);
+          mbar_arrive_expect_tx(&bars[slot], PLANE_BYTES);
+          tma_load_3d(ring + slot * Cfg::RING_PLANE, tm, X0, Y0, k + S, &bars[slot]);
+        }
       }
     }
   }
 }
 
-template <class SH, int T, int CY, int CX, int NWY, int S, bool DEC, bool EXACT, int MINB>
+template <class SH, int T, int CY, int CX, int NWY, int S, int FL, bool EXACT, bool UNI, int MINB>
 __global__ void __launch_bounds__(NWY * 32, MINB)
     k_stream3d(const __grid_constant__ TmapSet maps, const Stream3DArgs a,
                const __grid_constant__ Coefs<SH::NT> cf) {
-  using Cfg = Stream3DCfg<SH, T, CY, CX, NWY, S, DEC>;
+  using Cfg = Stream3DCfg<SH, T, CY, CX, NWY, S, FL>;
   constexpr int R = Cfg::R;
   extern __shared__ __align__(1024) unsigned char smem[];
   double* ring = reinterpret_cast<double*>(smem);
@@ -355,6 +390,7 @@ __global__ void __launch_bounds__(NWY * 32, MINB)
   if (threadIdx.x == 0) {
 #pragma unroll
     for (int i = 0; i < S; ++i) mbar_init(&bars[i], 1);
+    mbar_init(&bars[S], NWY * 32);
     fence_mbarrier_init();
     prefetch_tmap(&maps.m[0]);
     prefetch_tmap(&maps.m[1]);
@@ -365,6 +401,7 @@ __global__ void __launch_bounds__(NWY * 32, MINB)
   const int n0 = a.n0, n1 = a.n1, n2 = a.n2;
   const int units = a.nty * a.ntx * a.nseg;
   uint32_t ring_cnt = 0;
+  uint32_t adv = 0;  // advances completed by this CTA (split-phase barrier)
   int src = a.first_src, dst = a.first_dst;
   for (int e = 0; e < a.epochs; ++e) {
     const CUtensorMap* tm = &maps.m[src];
@@ -388,11 +425,11 @@ __global__ void __launch_bounds__(NWY * 32, MINB)
                         ((ty + 1) * Cfg::VY + TR > n1 - R) || (tx * Cfg::VX - TR < R) ||
                         ((tx + 1) * Cfg::VX + TR > n2 - R);
       if (edge)
-        stream3d_unit<SH, T, CY, CX, NWY, S, DEC, EXACT, true>(tm, out, ring, halo, bars, ring_cnt,
+        stream3d_unit<SH, T, CY, CX, NWY, S, FL, EXACT, UNI, true>(tm, out, ring, halo, bars, ring_cnt, adv,
                                                           warp, lane, n0, n1, n2, X0, Y0, r0,
                                                           r1, cf);
       else
-        stream3d_unit<SH, T, CY, CX, NWY, S, DEC, EXACT, false>(tm, out, ring, halo, bars, ring_cnt,
+        stream3d_unit<SH, T, CY, CX, NWY, S, FL, EXACT, UNI, false>(tm, out, ring, halo, bars, ring_cnt, adv,
                                                            warp, lane, n0, n1, n2, X0, Y0, r0,
                                                            r1, cf);
       ring_cnt += (uint32_t)(min(n0, r1 + TR) - max(0, r0 - TR));

@@ -10,10 +10,10 @@
 
 namespace ebisu {
 
-template <class SH, int T, int C, int NW, int S, bool EXACT, int MINB>
+template <class SH, int T, int C, int NW, int S, bool EXACT, bool UNI, int MINB>
 cudaError_t launch_stream2d(const TbLaunch& L) {
   using Cfg = Stream2DCfg<SH, T, C, NW, S>;
-  auto kern = k_stream2d<SH, T, C, NW, S, EXACT, MINB>;
+  auto kern = k_stream2d<SH, T, C, NW, S, EXACT, UNI, MINB>;
   cudaError_t err =
       cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg::SMEM_BYTES);
   if (err != cudaSuccess) return err;
@@ -43,28 +43,31 @@ cudaError_t launch_stream2d(const TbLaunch& L) {
   return cudaGetLastError();
 }
 
-// Register-budget heuristic: the window holds ~T*2R*C doubles live.
+// Register-budget heuristic: the windows hold T*(2R+1)*C doubles (2 registers
+// each) plus ~64 registers of addressing, halos and accumulators.  (The old
+// estimate 4*T*R*C+48 capped t=4..7 at 128/168 registers and spilled.)
 #ifndef EBISU_MINB_BIAS
 #define EBISU_MINB_BIAS 0
 #endif
 constexpr int s2d_minb(int T, int R, int C, int NW) {
-  const int est = 4 * T * R * C + 48;
+  const int est = 2 * T * (2 * R + 1) * C + 64;
   int m = 65536 / (NW * 32 * (est < 64 ? 64 : est)) + EBISU_MINB_BIAS;
   return m < 1 ? 1 : (m > 8 ? 8 : m);
 }
 
-#define EBISU_S2D_ENTRY(SHAPE_ID, SH, T, C, NW, S, EX)                                         \
+#define EBISU_S2D_ENTRY(SHAPE_ID, SH, T, C, NW, S, EX, UNI)                                    \
   TbKernel {                                                                                  \
-    SHAPE_ID, 2, T, C, NW, S, EX, Stream2DCfg<SH, T, C, NW, S>::SMEM_BYTES, 32 * C, 1, 1,      \
+    SHAPE_ID, 2, T, C, NW, S, EX, UNI, Stream2DCfg<SH, T, C, NW, S>::SMEM_BYTES, 32 * C, 1, 1, \
         Stream2DCfg<SH, T, C, NW, S>::VW, 0,                                                  \
-        (const void*)&k_stream2d<SH, T, C, NW, S, (EX) != 0, s2d_minb(T, SH::R, C, NW)>,      \
-        &launch_stream2d<SH, T, C, NW, S, (EX) != 0, s2d_minb(T, SH::R, C, NW)>               \
+        (const void*)&k_stream2d<SH, T, C, NW, S, (EX) != 0, (UNI) != 0,                      \
+                                 s2d_minb(T, SH::R, C, NW)>,                                  \
+        &launch_stream2d<SH, T, C, NW, S, (EX) != 0, (UNI) != 0, s2d_minb(T, SH::R, C, NW)>   \
   }
 
-template <class SH, int T, int CY, int CX, int NWY, int S, bool DEC, bool EXACT, int MINB>
+template <class SH, int T, int CY, int CX, int NWY, int S, int FL, bool EXACT, bool UNI, int MINB>
 cudaError_t launch_stream3d(const TbLaunch& L) {
-  using Cfg = Stream3DCfg<SH, T, CY, CX, NWY, S, DEC>;
-  auto kern = k_stream3d<SH, T, CY, CX, NWY, S, DEC, EXACT, MINB>;
+  using Cfg = Stream3DCfg<SH, T, CY, CX, NWY, S, FL>;
+  auto kern = k_stream3d<SH, T, CY, CX, NWY, S, FL, EXACT, UNI, MINB>;
   cudaError_t err =
       cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg::SMEM_BYTES);
   if (err != cudaSuccess) return err;
@@ -94,14 +97,14 @@ cudaError_t launch_stream3d(const TbLaunch& L) {
   return cudaGetLastError();
 }
 
-#define EBISU_S3D_ENTRY(SHAPE_ID, SH, T, CY, CX, NWY, S, DEC, EX, MINB)                         \
+#define EBISU_S3D_ENTRY(SHAPE_ID, SH, T, CY, CX, NWY, S, FL, EX, UNI, MINB)                    \
   TbKernel {                                                                                  \
-    SHAPE_ID, 3, T, CX, NWY, S, EX, Stream3DCfg<SH, T, CY, CX, NWY, S, DEC>::SMEM_BYTES,       \
-        Stream3DCfg<SH, T, CY, CX, NWY, S, DEC>::LX, Stream3DCfg<SH, T, CY, CX, NWY, S, DEC>::LY, \
-        1, Stream3DCfg<SH, T, CY, CX, NWY, S, DEC>::VX,                                        \
-        Stream3DCfg<SH, T, CY, CX, NWY, S, DEC>::VY,                                           \
-        (const void*)&k_stream3d<SH, T, CY, CX, NWY, S, DEC, (EX) != 0, MINB>,                \
-        &launch_stream3d<SH, T, CY, CX, NWY, S, DEC, (EX) != 0, MINB>                         \
+    SHAPE_ID, 3, T, CX, NWY, S, EX, UNI, Stream3DCfg<SH, T, CY, CX, NWY, S, FL>::SMEM_BYTES,  \
+        Stream3DCfg<SH, T, CY, CX, NWY, S, FL>::LX, Stream3DCfg<SH, T, CY, CX, NWY, S, FL>::LY, \
+        1, Stream3DCfg<SH, T, CY, CX, NWY, S, FL>::VX,                                        \
+        Stream3DCfg<SH, T, CY, CX, NWY, S, FL>::VY,                                           \
+        (const void*)&k_stream3d<SH, T, CY, CX, NWY, S, FL, (EX) != 0, (UNI) != 0, MINB>,    \
+        &launch_stream3d<SH, T, CY, CX, NWY, S, FL, (EX) != 0, (UNI) != 0, MINB>             \
   }
 
 }  // namespace ebisu

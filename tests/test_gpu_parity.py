@@ -128,6 +128,33 @@ def test_3d_shapes_all_depths_ragged(name):
             assert np.array_equal(out.cells, ref), (name, t, (n0, n1, n2), steps, tr)
 
 
+def _variants(st, t, ext, steps):
+    """Yield (variant, trace, output) for every registered kernel variant."""
+    g = eb.random_grid(ext, 97 + t)
+    for v in range(64):
+        prm = _native.make_params(t=t, variant=v)
+        try:
+            out, tr = eb.sweep(g, st, steps, params=prm, trace=True)
+        except Exception as e:  # past the last registered variant
+            assert "variant" in str(e), e
+            return
+        yield g, v, tr, out
+
+
+@pytest.mark.parametrize("name", list(CASES_3D))
+def test_3d_every_registered_variant_bitwise(name):
+    st = _shape(name)
+    for t in CASES_3D[name]:
+        steps = 3 * t + 1
+        for ext in ((37, 71, 134), (2 * st.radius + 3, 300, 66)):
+            ref = None
+            for g, v, tr, out in _variants(st, t, ext, steps):
+                if ref is None:
+                    ref = oracle_run(g.cells, taps_of(st), steps)
+                assert tr["kernel"] == "stream3d_tb", tr
+                assert np.array_equal(out.cells, ref), (name, t, v, ext, tr)
+
+
 def test_3d_lane_variants_and_persistence():
     st = _shape("j3d7pt")
     g = eb.random_grid((40, 70, 134), 11)
