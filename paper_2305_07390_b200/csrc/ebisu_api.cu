@@ -307,6 +307,11 @@ struct Counters {
   int grid = 0, nw = 0, t_used = 0, kid = KID_NONE;
 };
 
+inline int stream3d_advances_host(int ka, int r1, int TZ, int WN) {
+  const int n = r1 + TZ - ka;
+  return (n + WN - 1) / WN * WN;
+}
+
 // Row (axis-0) segmentation of the work units.  Every unit pays a pipeline
 // warm-up of `warm` advances; units are handed out dynamically to `slots`
 // concurrent workers, so an epoch takes about units*(len+warm)/slots plus a
@@ -460,14 +465,35 @@ int run_tb3d_stage(const ProblemDesc& p, const TbKernel* k, int epochs, int firs
   const int max_ctas = per_sm * di.sms;
   const int ntx = (n2 + k->valid_x - 1) / k->valid_x;
   const int nty = (n1 + k->valid_y - 1) / k->valid_y;
+  const long long tiles = (long long)ntx * nty;
   int nseg = 1, seg_len = n0;
-  plan_segments(n0, (long long)ntx * nty, max_ctas, 3 * T * R, std::max(8, 2 * T * R), &nseg,
-                &seg_len);
+  plan_segments(n0, tiles, max_ctas, 3 * T * R, std::max(8, 2 * T * R), &nseg, &seg_len);
+  std::vector<int> seg_start;
   if (seg_rows_req > 0) {
     seg_len = seg_rows_req;
-    nseg = (n0 + seg_len - 1) / seg_len;
+    for (int r = 0; r < n0; r += seg_len) seg_start.push_back(r);
+  } else {
+    // Guided schedule: start with the balanced length and halve it once the
+    // remaining work is under two rounds of units, so the epoch tail (the
+    // grid.sync wait) is made of short units.
+    const int min_len = std::max(8, 2 * T * R);
+    int cur = std::max(seg_len, min_len), pos = 0;
+    while (pos < n0) {
+      const long long rem = n0 - pos;
+      while (cur > min_len && rem * tiles < 2ll * cur * max_ctas) cur = std::max(min_len, cur / 2);
+      seg_start.push_back(pos);
+      pos += (int)std::min<long long>(cur, rem);
+    }
   }
-  const long long units = (long long)ntx * nty * nseg;
+  if ((int)seg_start.size() > EBISU_MAX_SEGS) {
+    // too fine: fall back to uniform segments within the table
+    seg_len = (n0 + EBISU_MAX_SEGS - 1) / EBISU_MAX_SEGS;
+    seg_start.clear();
+    for (int r = 0; r < n0; r += seg_len) seg_start.push_back(r);
+  }
+  nseg = (int)seg_start.size();
+  seg_start.push_back(n0);
+  const long long units = tiles * nseg;
   int grid = (int)std::min<long long>(max_ctas, units);
   if (grid < 1) grid = 1;
   const bool coop = coop_req && di.coop && epochs > 1;
@@ -479,6 +505,7 @@ int run_tb3d_stage(const ProblemDesc& p, const TbKernel* k, int epochs, int firs
   L.nty = nty;
   L.nseg = nseg;
   L.seg_len = seg_len;
+  L.seg_start = seg_start.data();
   for (int i = 0; i < 3; ++i) L.buf[i] = bufs[i];
   L.maps = maps;
   L.coeffs = p.coeffs;
@@ -511,11 +538,13 @@ int run_tb3d_stage(const ProblemDesc& p, const TbKernel* k, int epochs, int firs
   }
   cudaFreeAsync(work, st);
   uint64_t loads = 0, adv = 0;
+  const int WN = k->wn;
   for (int g = 0; g < nseg; ++g) {
-    const int r0 = g * seg_len, r1 = std::min(n0, r0 + seg_len);
-    const int ka = std::max(0, r0 - T * R), kb = std::min(n0, r1 + T * R);
-    loads += (uint64_t)(kb - ka);
-    adv += (uint64_t)(r1 + T * R - ka);
+    const int r0 = seg_start[g], r1 = seg_start[g + 1];
+    const int ka = std::max(0, r0 - T * R);
+    const int n = stream3d_advances_host(ka, r1, T * k->z, WN);
+    loads += (uint64_t)n;  // every advance loads one plane (TMA zero-fills past n0)
+    adv += (uint64_t)n;
   }
   const uint64_t tile_cells = (uint64_t)k->box0 * (uint64_t)k->box1;
   ctr->gm_loads += (uint64_t)epochs * loads * tile_cells * (uint64_t)ntx * nty;

@@ -11,6 +11,9 @@ namespace ebisu {
 
 constexpr unsigned kFullMask = 0xffffffffu;
 
+// Upper bound on axis-0 segments of one sweep (kernel-parameter table).
+#define EBISU_MAX_SEGS 96
+
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
   return static_cast<uint32_t>(__cvta_generic_to_shared(p));
 }

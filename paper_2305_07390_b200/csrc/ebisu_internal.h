@@ -45,6 +45,7 @@ struct TbLaunch {
   int nstrips, nseg, seg_len;  // 2-D decomposition
   int aligned;                 // 2-D: edge-aligned strips
   int ntx, nty;                // 3-D decomposition (tiles along axis 2 / axis 1)
+  const int* seg_start;        // 3-D: nseg+1 segment bounds along axis 0 (guided)
   int epochs;
   int first_src, first_dst;
   double* buf[3];
@@ -70,6 +71,8 @@ struct TbKernel {
   int box0, box1, box2;  // TMA box (elements) fastest first
   int valid_x;           // valid columns per warp strip (2-D) or per tile (3-D, axis 2)
   int valid_y;           // 3-D: valid rows per tile (axis 1)
+  int z;                 // 3-D: level skew along axis 0 (advances per level)
+  int wn;                // 3-D: window planes (advance-loop unroll)
   const void* func;      // kernel symbol (occupancy queries / attributes)
   cudaError_t (*launch)(const TbLaunch&);
 };

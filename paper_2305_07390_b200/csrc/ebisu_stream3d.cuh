@@ -35,7 +35,11 @@ struct Stream3DArgs {
   int n0, n1, n2;   // extents; plane pitch n1*n2, row pitch n2
   int nty, ntx;     // tiles along axis 1 / axis 2
   int nseg;         // z segments
-  int seg_len;
+  int seg_len;      // (planner's nominal length; the real bounds are seg_start)
+  // z segment j covers planes [seg_start[j], seg_start[j+1]).  Guided
+  // schedule: segments shrink toward the end of the list, and units are
+  // handed out segment-major, so the epoch tail is made of short units.
+  int seg_start[EBISU_MAX_SEGS + 1];
   int epochs;
   int first_src, first_dst;
   double* buf[3];
@@ -92,11 +96,7 @@ struct Stream3DCfg {
   static constexpr int RING_PLANE = LY * LX;          // doubles per ring slot
   static constexpr int RING_BYTES = S * RING_PLANE * 8;
   static constexpr int HALO_BYTES = T * NB * HPLANE * 8;
-  static constexpr int SMEM_BYTES = RING_BYTES + HALO_BYTES + (S + 1) * 8;
-  // FL bit 1 (SPLIT): the per-advance __syncthreads becomes a split-phase
-  // mbarrier (every thread arrives after its pushes; pulls of advance k wait
-  // for phase k-1), so warps drift by up to one advance instead of draining.
-  static constexpr bool SPLIT = (FL & 2) != 0;
+  static constexpr int SMEM_BYTES = RING_BYTES + HALO_BYTES + S * 8;
   static_assert(CY >= R, "a warp's rows must cover the radius");
   static_assert(VY > 0 && VX > 0, "tile leaves no valid core");
   static_assert(LX <= 256 && LY <= 256, "TMA box dims are limited to 256");
@@ -104,44 +104,62 @@ struct Stream3DCfg {
   static_assert(SMEM_BYTES <= 227 * 1024, "shared memory budget");
 };
 
+// Advances of a unit: [ka, ka + nadv), nadv rounded up to a multiple of WN so
+// the unrolled loop never runs past the planes it loaded.  Planes >= n0 come
+// back zero-filled from TMA; planes in [r1 + T*R, ka + nadv) only feed target
+// planes >= r1, which are never stored.
+template <int WN>
+__host__ __device__ inline int stream3d_advances(int ka, int r1, int TZ) {
+  const int n = r1 + TZ - ka;
+  return (n + WN - 1) / WN * WN;
+}
+
+// One work unit (tile x z segment) of one epoch.  EDGE: the tile touches the
+// frame along axis 1 or 2 (per-cell frame masks); frame planes along axis 0
+// are handled per block of WN advances (FPL), so z-edge segments cost the same
+// as interior ones outside their first and last blocks.  Returns the planes
+// consumed from the ring.
 template <class SH, int T, int CY, int CX, int NWY, int S, int FL, bool EXACT, bool UNI, bool EDGE>
-__device__ __forceinline__ void stream3d_unit(const CUtensorMap* tm, double* __restrict__ out,
-                                              double* ring, double* halo, uint64_t* bars,
-                                              uint32_t ring_cnt, uint32_t& adv, int warp,
-                                              int lane, int n0,
-                                              int n1, int n2, int X0, int Y0, int r0, int r1,
-                                              const Coefs<SH::NT>& cf) {
+__device__ __forceinline__ int stream3d_unit(const CUtensorMap* tm, double* __restrict__ out,
+                                             double* ring, double* halo, uint64_t* bars,
+                                             uint32_t ring_cnt, int warp, int lane, int n0,
+                                             int n1, int n2, int X0, int Y0, int r0, int r1,
+                                             const Coefs<SH::NT>& cf) {
   using Cfg = Stream3DCfg<SH, T, CY, CX, NWY, S, FL>;
   constexpr int R = Cfg::R, Z = Cfg::Z, WN = Cfg::WN, NB = Cfg::NB;
   constexpr int LY = Cfg::LY, LX = Cfg::LX, HY = Cfg::HY, HX = Cfg::HX;
   constexpr int PLANE_BYTES = LY * LX * 8;
   constexpr int TZ = T * Z;  // pipeline depth along z
+  static_assert(CY * CX <= 32, "cell masks are 32-bit");
 
   const int ka = max(0, r0 - T * R);
-  const int kb = min(n0, r1 + T * R);
-  const int kend = r1 + TZ;
+  const int nadv = stream3d_advances<WN>(ka, r1, TZ);
+  const int kend = ka + nadv;
   const int tid = warp * 32 + lane;
   const int ty0 = warp * CY;  // tile row of this thread's first row
   const int tx0 = lane * CX;  // tile column of this thread's first column
 
   if (tid == 0) {
-    for (int i = 0; i < S && ka + i < kb; ++i) {
+    for (int i = 0; i < S && i < nadv; ++i) {
       const uint32_t slot = (ring_cnt + i) & (S - 1);
       mbar_arrive_expect_tx(&bars[slot], PLANE_BYTES);
       tma_load_3d(ring + slot * Cfg::RING_PLANE, tm, X0, Y0, ka + i, &bars[slot]);
     }
   }
 
-  bool fcell[CY][CX];
-  bool stcell[CY][CX];
+  // per-cell masks, bit cy*CX+cx: frame cells (EDGE tiles) and stored cells
+  uint32_t fmask = 0, stmask = 0;
 #pragma unroll
   for (int cy = 0; cy < CY; ++cy)
 #pragma unroll
     for (int cx = 0; cx < CX; ++cx) {
       const int yy = Y0 + ty0 + cy, xx = X0 + tx0 + cx;
-      fcell[cy][cx] = EDGE && ((yy < R) || (yy >= n1 - R) || (xx < R) || (xx >= n2 - R));
-      stcell[cy][cx] = (ty0 + cy >= HY) && (ty0 + cy < LY - HY) && (tx0 + cx >= HX) &&
-                       (tx0 + cx < LX - HX) && (yy < n1) && (xx < n2);
+      const bool f = EDGE && ((yy < R) || (yy >= n1 - R) || (xx < R) || (xx >= n2 - R));
+      bool st = (ty0 + cy >= HY) && (ty0 + cy < LY - HY) && (tx0 + cx >= HX) &&
+                (tx0 + cx < LX - HX) && (yy < n1) && (xx < n2);
+      if (UNI) st = st && !f;  // shared-product levels hold products; frame pre-copied
+      fmask |= (uint32_t)f << (cy * CX + cx);
+      stmask |= (uint32_t)st << (cy * CX + cx);
     }
 
   double win[T][WN][CY][CX];
@@ -180,49 +198,36 @@ __device__ __forceinline__ void stream3d_unit(const CUtensorMap* tm, double* __r
   const int wa = warp > 0 ? warp - 1 : warp;
   const int wbl = warp < NWY - 1 ? warp + 1 : warp;
 
-  for (int kbase = ka; kbase < kend; kbase += WN) {
+  // output pointer of this thread's first cell in plane q = k - T*Z
+  const long long plane = (long long)n1 * (long long)n2;
+  double* obase = out + ((long long)(Y0 + ty0) * n2 + (X0 + tx0));
+
+  auto block = [&](int kbase, auto fpl_tag) {
+    constexpr bool FPL = decltype(fpl_tag)::value;  // a target plane may be a frame plane
 #pragma unroll
     for (int uu = 0; uu < WN; ++uu) {
       const int k = kbase + uu;
       const int bk = k % NB;  // halo buffer written this advance
-      if constexpr (Cfg::SPLIT) {
-        // all pushes of the previous advance visible; all its ring reads done
-        if (adv > 0) mbar_wait(&bars[S], (adv - 1) & 1);
-        const int kp = k - 1;
-        if (tid == 0 && kp >= ka && kp < kb && kp + S < kb) {
-          const uint32_t pos = ring_cnt + (uint32_t)(kp - ka);
-          const uint32_t slot = pos & (S - 1);
-          mbar_arrive_expect_tx(&bars[slot], PLANE_BYTES);
-          tma_load_3d(ring + slot * Cfg::RING_PLANE, tm, X0, Y0, kp + S, &bars[slot]);
-        }
-      }
       // ---- level 0 ----------------------------------------------------------
       {
         double v[CY][CX];
-        if (k < kb) {
-          const uint32_t pos = ring_cnt + (uint32_t)(k - ka);
-          const uint32_t slot = pos & (S - 1);
-          mbar_wait(&bars[slot], (pos / S) & 1);
-          const double* p = ring + slot * Cfg::RING_PLANE + ty0 * LX + tx0;
+        const uint32_t pos = ring_cnt + (uint32_t)(k - ka);
+        const uint32_t slot = pos & (S - 1);
+        mbar_wait(&bars[slot], (pos / S) & 1);
+        const double* p = ring + slot * Cfg::RING_PLANE + ty0 * LX + tx0;
 #pragma unroll
-          for (int cy = 0; cy < CY; ++cy) {
-            if constexpr (CX % 2 == 0) {
+        for (int cy = 0; cy < CY; ++cy) {
+          if constexpr (CX % 2 == 0) {
 #pragma unroll
-              for (int cx = 0; cx < CX; cx += 2) {
-                const double2 t2 = *reinterpret_cast<const double2*>(p + cy * LX + cx);
-                v[cy][cx] = t2.x;
-                v[cy][cx + 1] = t2.y;
-              }
-            } else {
-#pragma unroll
-              for (int cx = 0; cx < CX; ++cx) v[cy][cx] = p[cy * LX + cx];
+            for (int cx = 0; cx < CX; cx += 2) {
+              const double2 t2 = *reinterpret_cast<const double2*>(p + cy * LX + cx);
+              v[cy][cx] = t2.x;
+              v[cy][cx + 1] = t2.y;
             }
+          } else {
+#pragma unroll
+            for (int cx = 0; cx < CX; ++cx) v[cy][cx] = p[cy * LX + cx];
           }
-        } else {
-#pragma unroll
-          for (int cy = 0; cy < CY; ++cy)
-#pragma unroll
-            for (int cx = 0; cx < CX; ++cx) v[cy][cx] = 0.0;
         }
         // UNI: windows and halos carry products y = c*x (one DMUL per cell)
         if constexpr (UNI) {
@@ -241,11 +246,9 @@ __device__ __forceinline__ void stream3d_unit(const CUtensorMap* tm, double* __r
       static_for<T>([&](auto sI) {
         constexpr int s = decltype(sI)::value + 1;
         const int q = k - s * Z;  // target plane of level s
+        bool fpl = false;         // frame plane: every cell carries level s-1
+        if constexpr (FPL) fpl = (q < R) || (q >= n0 - R);
         double nv[CY][CX];
-        // frame plane / frame cell: value carries over from level s-1 (selects,
-        // not branches, so all levels stay in one basic block)
-        bool frame_plane = false;
-        if constexpr (EDGE) frame_plane = (q < R) || (q >= n0 - R);
         {
           // extended neighbourhood of the planes that need in-plane values:
           // ext[dz][cy+R][cx+R], cy in [-R, CY+R), cx in [-R, CX+R)
@@ -331,12 +334,13 @@ __device__ __forceinline__ void stream3d_unit(const CUtensorMap* tm, double* __r
               // changes, and level T skips frame cells (host pre-copies them)
               const double val =
                   (UNI && s < T) ? __dmul_rn(cf.c[0], acc[cy][cx]) : acc[cy][cx];
-              if constexpr (EDGE)
-                nv[cy][cx] = (frame_plane || fcell[cy][cx])
-                                 ? win[s - 1][pmod<WN>(uu - s * Z)][cy][cx]
-                                 : val;
-              else
+              if constexpr (EDGE || FPL) {
+                bool f = fpl;
+                if constexpr (EDGE) f = f || ((fmask >> (cy * CX + cx)) & 1u);
+                nv[cy][cx] = f ? win[s - 1][pmod<WN>(uu - s * Z)][cy][cx] : val;
+              } else {
                 nv[cy][cx] = val;
+              }
             }
         }
         if constexpr (s < T) {
@@ -346,33 +350,36 @@ __device__ __forceinline__ void stream3d_unit(const CUtensorMap* tm, double* __r
             for (int cx = 0; cx < CX; ++cx) win[s][pmod<WN>(uu - s * Z)][cy][cx] = nv[cy][cx];
           push(s, bk, nv);
         } else {
-          if (q >= r0 && q < r1) {
-            const long long base =
-                ((long long)q * n1 + (long long)(Y0 + ty0)) * (long long)n2 + (X0 + tx0);
+          bool qok = (q >= r0) && (q < r1);
+          if (UNI && FPL) qok = qok && !fpl;
+          if (qok) {
+            double* o = obase + (long long)q * plane;
 #pragma unroll
             for (int cy = 0; cy < CY; ++cy)
 #pragma unroll
               for (int cx = 0; cx < CX; ++cx)
-                if (stcell[cy][cx] && !(UNI && EDGE && (frame_plane || fcell[cy][cx])))
-                  out[base + (long long)cy * n2 + cx] = nv[cy][cx];
+                if ((stmask >> (cy * CX + cx)) & 1u) o[(long long)cy * n2 + cx] = nv[cy][cx];
           }
         }
       });
-      if constexpr (Cfg::SPLIT) {
-        mbar_arrive(&bars[S]);
-        ++adv;
-      } else {
-        // one barrier per advance: halo pushes visible, ring slot k consumed
-        __syncthreads();
-        if (tid == 0 && k < kb && k + S < kb) {
-          const uint32_t pos = ring_cnt + (uint32_t)(k - ka);
-          const uint32_t slot = pos & (S - 1);
-          mbar_arrive_expect_tx(&bars[slot], PLANE_BYTES);
-          tma_load_3d(ring + slot * Cfg::RING_PLANE, tm, X0, Y0, k + S, &bars[slot]);
-        }
+      // one barrier per advance: halo pushes visible, ring slot k consumed
+      __syncthreads();
+      if (tid == 0 && k + S < kend) {
+        const uint32_t slot = (ring_cnt + (uint32_t)(k - ka)) & (S - 1);
+        mbar_arrive_expect_tx(&bars[slot], PLANE_BYTES);
+        tma_load_3d(ring + slot * Cfg::RING_PLANE, tm, X0, Y0, k + S, &bars[slot]);
       }
     }
+  };
+
+  for (int kbase = ka; kbase < kend; kbase += WN) {
+    // target planes of this block: [kbase - TZ, kbase + WN - 1 - Z]
+    if ((kbase - TZ < R) || (kbase + WN - 1 - Z >= n0 - R))
+      block(kbase, std::true_type{});
+    else
+      block(kbase, std::false_type{});
   }
+  return nadv;
 }
 
 template <class SH, int T, int CY, int CX, int NWY, int S, int FL, bool EXACT, bool UNI, int MINB>
@@ -390,7 +397,6 @@ __global__ void __launch_bounds__(NWY * 32, MINB)
   if (threadIdx.x == 0) {
 #pragma unroll
     for (int i = 0; i < S; ++i) mbar_init(&bars[i], 1);
-    mbar_init(&bars[S], NWY * 32);
     fence_mbarrier_init();
     prefetch_tmap(&maps.m[0]);
     prefetch_tmap(&maps.m[1]);
@@ -399,9 +405,9 @@ __global__ void __launch_bounds__(NWY * 32, MINB)
   __syncthreads();
 
   const int n0 = a.n0, n1 = a.n1, n2 = a.n2;
-  const int units = a.nty * a.ntx * a.nseg;
+  const int tiles = a.nty * a.ntx;
+  const int units = tiles * a.nseg;
   uint32_t ring_cnt = 0;
-  uint32_t adv = 0;  // advances completed by this CTA (split-phase barrier)
   int src = a.first_src, dst = a.first_dst;
   for (int e = 0; e < a.epochs; ++e) {
     const CUtensorMap* tm = &maps.m[src];
@@ -413,26 +419,27 @@ __global__ void __launch_bounds__(NWY * 32, MINB)
       __syncthreads();
       const int u = s_unit;
       if (u >= units) break;
-      const int tx = u % a.ntx;
-      const int ty = (u / a.ntx) % a.nty;
-      const int seg = u / (a.ntx * a.nty);
+      // segment-major order: the long segments are handed out first and the
+      // short tail segments last (guided scheduling, see Stream3DArgs)
+      const int j = u / tiles;
+      const int tile = u - j * tiles;
+      const int tx = tile % a.ntx;
+      const int ty = tile / a.ntx;
+      const int r0 = a.seg_start[j];
+      const int r1 = a.seg_start[j + 1];
       const int X0 = tx * Cfg::VX - Cfg::HX;
       const int Y0 = ty * Cfg::VY - Cfg::HY;
-      const int r0 = seg * a.seg_len;
-      const int r1 = min(n0, r0 + a.seg_len);
       const int TR = T * R;
-      const bool edge = (r0 - TR < R) || (r1 + TR > n0 - R) || (ty * Cfg::VY - TR < R) ||
-                        ((ty + 1) * Cfg::VY + TR > n1 - R) || (tx * Cfg::VX - TR < R) ||
-                        ((tx + 1) * Cfg::VX + TR > n2 - R);
+      const bool edge = (ty * Cfg::VY - TR < R) || ((ty + 1) * Cfg::VY + TR > n1 - R) ||
+                        (tx * Cfg::VX - TR < R) || ((tx + 1) * Cfg::VX + TR > n2 - R);
+      int used;
       if (edge)
-        stream3d_unit<SH, T, CY, CX, NWY, S, FL, EXACT, UNI, true>(tm, out, ring, halo, bars, ring_cnt, adv,
-                                                          warp, lane, n0, n1, n2, X0, Y0, r0,
-                                                          r1, cf);
+        used = stream3d_unit<SH, T, CY, CX, NWY, S, FL, EXACT, UNI, true>(
+            tm, out, ring, halo, bars, ring_cnt, warp, lane, n0, n1, n2, X0, Y0, r0, r1, cf);
       else
-        stream3d_unit<SH, T, CY, CX, NWY, S, FL, EXACT, UNI, false>(tm, out, ring, halo, bars, ring_cnt, adv,
-                                                           warp, lane, n0, n1, n2, X0, Y0, r0,
-                                                           r1, cf);
-      ring_cnt += (uint32_t)(min(n0, r1 + TR) - max(0, r0 - TR));
+        used = stream3d_unit<SH, T, CY, CX, NWY, S, FL, EXACT, UNI, false>(
+            tm, out, ring, halo, bars, ring_cnt, warp, lane, n0, n1, n2, X0, Y0, r0, r1, cf);
+      ring_cnt += (uint32_t)used;
       __syncthreads();  // halo buffers and s_unit are reused by the next unit
     }
     if (e + 1 < a.epochs) {

@@ -58,7 +58,7 @@ constexpr int s2d_minb(int T, int R, int C, int NW) {
 #define EBISU_S2D_ENTRY(SHAPE_ID, SH, T, C, NW, S, EX, UNI)                                    \
   TbKernel {                                                                                  \
     SHAPE_ID, 2, T, C, NW, S, EX, UNI, Stream2DCfg<SH, T, C, NW, S>::SMEM_BYTES, 32 * C, 1, 1, \
-        Stream2DCfg<SH, T, C, NW, S>::VW, 0,                                                  \
+        Stream2DCfg<SH, T, C, NW, S>::VW, 0, 0, 0,                                            \
         (const void*)&k_stream2d<SH, T, C, NW, S, (EX) != 0, (UNI) != 0,                      \
                                  s2d_minb(T, SH::R, C, NW)>,                                  \
         &launch_stream2d<SH, T, C, NW, S, (EX) != 0, (UNI) != 0, s2d_minb(T, SH::R, C, NW)>   \
@@ -81,6 +81,8 @@ cudaError_t launch_stream3d(const TbLaunch& L) {
   a.ntx = L.ntx;
   a.nseg = L.nseg;
   a.seg_len = L.seg_len;
+  if (L.nseg > EBISU_MAX_SEGS) return cudaErrorInvalidValue;
+  for (int j = 0; j <= L.nseg; ++j) a.seg_start[j] = L.seg_start[j];
   a.epochs = L.epochs;
   a.first_src = L.first_src;
   a.first_dst = L.first_dst;
@@ -102,7 +104,8 @@ cudaError_t launch_stream3d(const TbLaunch& L) {
     SHAPE_ID, 3, T, CX, NWY, S, EX, UNI, Stream3DCfg<SH, T, CY, CX, NWY, S, FL>::SMEM_BYTES,  \
         Stream3DCfg<SH, T, CY, CX, NWY, S, FL>::LX, Stream3DCfg<SH, T, CY, CX, NWY, S, FL>::LY, \
         1, Stream3DCfg<SH, T, CY, CX, NWY, S, FL>::VX,                                        \
-        Stream3DCfg<SH, T, CY, CX, NWY, S, FL>::VY,                                           \
+        Stream3DCfg<SH, T, CY, CX, NWY, S, FL>::VY, Stream3DCfg<SH, T, CY, CX, NWY, S, FL>::Z,  \
+        Stream3DCfg<SH, T, CY, CX, NWY, S, FL>::WN,                                           \
         (const void*)&k_stream3d<SH, T, CY, CX, NWY, S, FL, (EX) != 0, (UNI) != 0, MINB>,    \
         &launch_stream3d<SH, T, CY, CX, NWY, S, FL, (EX) != 0, (UNI) != 0, MINB>             \
   }
