@@ -382,6 +382,223 @@ __device__ __forceinline__ int stream3d_unit(const CUtensorMap* tm, double* __re
   return nadv;
 }
 
+// Radius-1 stars in catalog order ((-1,0,0), (0,0,0), (1,0,0), then in-plane
+// taps of the centre plane): the z window of 3 planes per level collapses to 2
+// values per cell -- the partial sum P = t(-1) + t(0) of the next target and
+// the newest plane Y (the next target's centre).  Same operations in the same
+// order, one third fewer window registers, no rotating window (unroll 1).
+template <class SH>
+__host__ __device__ constexpr bool ps_eligible() {
+  if (!(SH::kStar && SH::R == 1 && SH::dims == 3)) return false;
+  if (SH::tap(0).d0 != -1 || SH::tap(1).d0 != 0 || SH::tap(2).d0 != 1) return false;
+  for (int i = 0; i < 3; ++i)
+    if (SH::tap(i).d1 != 0 || SH::tap(i).d2 != 0) return false;
+  for (int i = 3; i < SH::NT; ++i)
+    if (SH::tap(i).d0 != 0) return false;
+  return true;
+}
+
+template <class SH, int T, int CY, int CX, int NWY, int S, int FL, bool EXACT, bool UNI, bool EDGE>
+__device__ __forceinline__ int stream3d_unit_ps(const CUtensorMap* tm, double* __restrict__ out,
+                                                double* ring, double* halo, uint64_t* bars,
+                                                uint32_t ring_cnt, int warp, int lane, int n0,
+                                                int n1, int n2, int X0, int Y0, int r0, int r1,
+                                                const Coefs<SH::NT>& cf) {
+  using Cfg = Stream3DCfg<SH, T, CY, CX, NWY, S, FL>;
+  static_assert(ps_eligible<SH>(), "partial-sum path needs a radius-1 star in catalog order");
+  constexpr int NB = Cfg::NB;
+  constexpr int LY = Cfg::LY, LX = Cfg::LX, HY = Cfg::HY, HX = Cfg::HX;
+  constexpr int PLANE_BYTES = LY * LX * 8;
+  static_assert(Cfg::Z == 1 && NB >= 2, "star skew");
+  static_assert(CY * CX <= 32, "cell masks are 32-bit");
+
+  const int ka = max(0, r0 - T);
+  // level T emits plane k - T; advances run in pairs (the rolling Y/P state
+  // then alternates between two register sets instead of being moved), and
+  // an extra trailing advance only targets planes >= r1
+  const int nadv = (r1 + T - ka + 1) & ~1;
+  const int kend = ka + nadv;
+  const int tid = warp * 32 + lane;
+  const int ty0 = warp * CY;
+  const int tx0 = lane * CX;
+
+  if (tid == 0) {
+    for (int i = 0; i < S && i < nadv; ++i) {
+      const uint32_t slot = (ring_cnt + i) & (S - 1);
+      mbar_arrive_expect_tx(&bars[slot], PLANE_BYTES);
+      tma_load_3d(ring + slot * Cfg::RING_PLANE, tm, X0, Y0, ka + i, &bars[slot]);
+    }
+  }
+
+  uint32_t fmask = 0, stmask = 0;
+#pragma unroll
+  for (int cy = 0; cy < CY; ++cy)
+#pragma unroll
+    for (int cx = 0; cx < CX; ++cx) {
+      const int yy = Y0 + ty0 + cy, xx = X0 + tx0 + cx;
+      const bool f = EDGE && ((yy < 1) || (yy >= n1 - 1) || (xx < 1) || (xx >= n2 - 1));
+      bool st = (ty0 + cy >= HY) && (ty0 + cy < LY - HY) && (tx0 + cx >= HX) &&
+                (tx0 + cx < LX - HX) && (yy < n1) && (xx < n2);
+      if (UNI) st = st && !f;
+      fmask |= (uint32_t)f << (cy * CX + cx);
+      stmask |= (uint32_t)st << (cy * CX + cx);
+    }
+
+  // Y[s]: newest plane of level s; P[s]: partial sum (taps 0 and 1) of level
+  // s+1's next target.  Level s+1 at advance k targets q = k-s-1, whose centre
+  // is Y[s] (produced last advance) and whose z+1 plane is produced now.
+  double Y[T][CY][CX], P[T][CY][CX];
+#pragma unroll
+  for (int s = 0; s < T; ++s)
+#pragma unroll
+    for (int cy = 0; cy < CY; ++cy)
+#pragma unroll
+      for (int cx = 0; cx < CX; ++cx) Y[s][cy][cx] = P[s][cy][cx] = 0.0;
+
+  auto hrow = [&](int level, int b, int w, int r) -> double* {
+    return halo + (size_t)(level * NB + b) * Cfg::HPLANE + (size_t)(w * 2 + r) * LX + tx0;
+  };
+  auto push = [&](int level, int b, const double (&v)[CY][CX]) {
+#pragma unroll
+    for (int r = 0; r < 2; ++r) {
+      const int cy = r == 0 ? 0 : CY - 1;
+      double* d = hrow(level, b, warp, r);
+#pragma unroll
+      for (int cx = 0; cx < CX; cx += 2)
+        *reinterpret_cast<double2*>(d + cx) = make_double2(v[cy][cx], v[cy][cx + 1]);
+    }
+  };
+  const int wa = warp > 0 ? warp - 1 : warp;
+  const int wbl = warp < NWY - 1 ? warp + 1 : warp;
+  const long long plane = (long long)n1 * (long long)n2;
+  double* obase = out + ((long long)(Y0 + ty0) * n2 + (X0 + tx0));
+
+  auto advance = [&](int k, auto fpl_tag) {
+    constexpr bool FPL = decltype(fpl_tag)::value;
+    const int bk = k & (NB - 1);        // halo buffer written this advance
+    const int bp = (k - 1) & (NB - 1);  // centre planes were pushed last advance
+    double nw[CY][CX];                  // newest plane of the level below
+    {
+      const uint32_t pos = ring_cnt + (uint32_t)(k - ka);
+      const uint32_t slot = pos & (S - 1);
+      mbar_wait(&bars[slot], (pos / S) & 1);
+      const double* p = ring + slot * Cfg::RING_PLANE + ty0 * LX + tx0;
+#pragma unroll
+      for (int cy = 0; cy < CY; ++cy)
+#pragma unroll
+        for (int cx = 0; cx < CX; cx += 2) {
+          const double2 t2 = *reinterpret_cast<const double2*>(p + cy * LX + cx);
+          nw[cy][cx] = UNI ? __dmul_rn(cf.c[0], t2.x) : t2.x;
+          nw[cy][cx + 1] = UNI ? __dmul_rn(cf.c[0], t2.y) : t2.y;
+        }
+      push(0, bk, nw);
+    }
+    static_for<T>([&](auto sI) {
+      constexpr int s = decltype(sI)::value + 1;  // level produced
+      const int q = k - s;
+      bool fpl = false;
+      if constexpr (FPL) fpl = (q < 1) || (q >= n0 - 1);
+      // centre plane of level s-1 with its in-plane halo
+      double ext[CY + 2][CX + 2];
+#pragma unroll
+      for (int cy = 0; cy < CY; ++cy)
+#pragma unroll
+        for (int cx = 0; cx < CX; ++cx) ext[cy + 1][cx + 1] = Y[s - 1][cy][cx];
+      {
+        const double* up = hrow(s - 1, bp, wa, warp > 0 ? 1 : 0);
+        const double* dn = hrow(s - 1, bp, wbl, warp < NWY - 1 ? 0 : 1);
+#pragma unroll
+        for (int cx = 0; cx < CX; cx += 2) {
+          const double2 a2 = *reinterpret_cast<const double2*>(up + cx);
+          const double2 b2 = *reinterpret_cast<const double2*>(dn + cx);
+          ext[0][cx + 1] = a2.x;
+          ext[0][cx + 2] = a2.y;
+          ext[CY + 1][cx + 1] = b2.x;
+          ext[CY + 1][cx + 2] = b2.y;
+        }
+      }
+#pragma unroll
+      for (int cy = 1; cy <= CY; ++cy) {
+        ext[cy][0] = __shfl_up_sync(kFullMask, ext[cy][CX], 1);
+        ext[cy][CX + 1] = __shfl_down_sync(kFullMask, ext[cy][1], 1);
+      }
+      double nv[CY][CX];
+#pragma unroll
+      for (int cy = 0; cy < CY; ++cy)
+#pragma unroll
+        for (int cx = 0; cx < CX; ++cx) {
+          double acc;
+          if constexpr (UNI)
+            acc = __dadd_rn(P[s - 1][cy][cx], nw[cy][cx]);
+          else
+            acc = tap_next<EXACT>(P[s - 1][cy][cx], cf.c[2], nw[cy][cx]);
+          static_for<SH::NT - 3>([&](auto iI) {
+            constexpr int i = decltype(iI)::value + 3;
+            constexpr Off o = SH::tap(i);
+            const double x = ext[cy + 1 + o.d1][cx + 1 + o.d2];
+            if constexpr (UNI)
+              acc = __dadd_rn(acc, x);
+            else
+              acc = tap_next<EXACT>(acc, cf.c[i], x);
+          });
+          const double val = (UNI && s < T) ? __dmul_rn(cf.c[0], acc) : acc;
+          if constexpr (EDGE || FPL) {
+            bool f = fpl;
+            if constexpr (EDGE) f = f || ((fmask >> (cy * CX + cx)) & 1u);
+            nv[cy][cx] = f ? Y[s - 1][cy][cx] : val;
+          } else {
+            nv[cy][cx] = val;
+          }
+        }
+      // roll level s-1's state: next target's first two taps, newest plane
+#pragma unroll
+      for (int cy = 0; cy < CY; ++cy)
+#pragma unroll
+        for (int cx = 0; cx < CX; ++cx) {
+          if constexpr (UNI)
+            P[s - 1][cy][cx] = __dadd_rn(Y[s - 1][cy][cx], nw[cy][cx]);
+          else
+            P[s - 1][cy][cx] = tap_next<EXACT>(tap_first<EXACT>(cf.c[0], Y[s - 1][cy][cx]),
+                                               cf.c[1], nw[cy][cx]);
+          Y[s - 1][cy][cx] = nw[cy][cx];
+          nw[cy][cx] = nv[cy][cx];
+        }
+      if constexpr (s < T) {
+        push(s, bk, nv);
+      } else {
+        bool qok = (q >= r0) && (q < r1);
+        if (UNI && FPL) qok = qok && !fpl;
+        if (qok) {
+          double* o = obase + (long long)q * plane;
+#pragma unroll
+          for (int cy = 0; cy < CY; ++cy)
+#pragma unroll
+            for (int cx = 0; cx < CX; ++cx)
+              if ((stmask >> (cy * CX + cx)) & 1u) o[(long long)cy * n2 + cx] = nv[cy][cx];
+        }
+      }
+    });
+    __syncthreads();
+    if (tid == 0 && k + S < kend) {
+      const uint32_t slot = (ring_cnt + (uint32_t)(k - ka)) & (S - 1);
+      mbar_arrive_expect_tx(&bars[slot], PLANE_BYTES);
+      tma_load_3d(ring + slot * Cfg::RING_PLANE, tm, X0, Y0, k + S, &bars[slot]);
+    }
+  };
+
+  for (int k = ka; k < kend; k += 2) {
+    // target planes of these two advances: [k - T, k]
+    if ((k - T < 1) || (k >= n0 - 1)) {
+      advance(k, std::true_type{});
+      advance(k + 1, std::true_type{});
+    } else {
+      advance(k, std::false_type{});
+      advance(k + 1, std::false_type{});
+    }
+  }
+  return nadv;
+}
+
 template <class SH, int T, int CY, int CX, int NWY, int S, int FL, bool EXACT, bool UNI, int MINB>
 __global__ void __launch_bounds__(NWY * 32, MINB)
     k_stream3d(const __grid_constant__ TmapSet maps, const Stream3DArgs a,
@@ -433,7 +650,14 @@ __global__ void __launch_bounds__(NWY * 32, MINB)
       const bool edge = (ty * Cfg::VY - TR < R) || ((ty + 1) * Cfg::VY + TR > n1 - R) ||
                         (tx * Cfg::VX - TR < R) || ((tx + 1) * Cfg::VX + TR > n2 - R);
       int used;
-      if (edge)
+      if constexpr (ps_eligible<SH>() && (FL & 1) == 0) {
+        if (edge)
+          used = stream3d_unit_ps<SH, T, CY, CX, NWY, S, FL, EXACT, UNI, true>(
+              tm, out, ring, halo, bars, ring_cnt, warp, lane, n0, n1, n2, X0, Y0, r0, r1, cf);
+        else
+          used = stream3d_unit_ps<SH, T, CY, CX, NWY, S, FL, EXACT, UNI, false>(
+              tm, out, ring, halo, bars, ring_cnt, warp, lane, n0, n1, n2, X0, Y0, r0, r1, cf);
+      } else if (edge)
         used = stream3d_unit<SH, T, CY, CX, NWY, S, FL, EXACT, UNI, true>(
             tm, out, ring, halo, bars, ring_cnt, warp, lane, n0, n1, n2, X0, Y0, r0, r1, cf);
       else

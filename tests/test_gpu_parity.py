@@ -205,6 +205,38 @@ def test_coefficients_are_runtime():
                           oracle_run(g.cells, taps_of(st), 9))
 
 
+PER_TAP_DEPTHS = {"j2d5pt": [1, 2, 4, 8], "j2d9pt-gol": [1, 2, 4, 8], "j2d9pt": [1, 2, 4],
+                  "j2d25pt": [1, 2, 3], "j2d13pt": [1, 2, 3], "j2ds25pt": [1, 2],
+                  "j3d7pt": [1, 2, 3, 4], "j3d27pt": [1, 2], "j3d13pt": [1, 2],
+                  "j3d17pt": [1, 2], "poisson": [1, 2]}
+
+
+@pytest.mark.parametrize("name", list(PER_TAP_DEPTHS))
+def test_per_tap_kernels_bitwise(name):
+    """The per-tap kernel family (non-uniform coefficients): forced with
+    per_tap_products=1 on the catalog coefficients and selected automatically
+    for non-uniform ones -- both bitwise against the oracle."""
+    base = _shape(name)
+    rng = eb.SplitMix64(7 + len(name))
+    coeffs = [0.05 + 0.9 * rng.uniform() / len(base.taps) for _ in base.taps]
+    nonuni = base.with_coefficients(coeffs)
+    r = base.radius
+    ext = (3 * r + 40, 2 * r + 70, 2 * (r + 30)) if base.dims == 3 else (2 * r + 150, 2 * (r + 160))
+    g = eb.random_grid(ext[:base.dims], 31)
+    for t in PER_TAP_DEPTHS[name]:
+        steps = 2 * t + 1
+        for st, forced in ((base, True), (nonuni, False)):
+            prm = _native.make_params(t=t, per_tap_products=forced)
+            out, tr = eb.sweep(g, st, steps, params=prm, trace=True)
+            assert tr["kernel"] in ("stream2d_tb", "stream3d_tb"), tr
+            ref = oracle_run(g.cells, taps_of(st), steps)
+            assert np.array_equal(out.cells, ref), (name, t, forced)
+        # FMA chain with non-uniform coefficients: tolerance, not bitwise
+        out = eb.sweep(g, nonuni, steps, params=_native.make_params(t=t, exact=False))
+        ref = oracle_run(g.cells, taps_of(nonuni), steps)
+        assert np.max(np.abs(out.cells - ref)) <= FMA_RTOL * np.max(np.abs(ref)), (name, t)
+
+
 def test_purity_and_boundary_tag():
     st = eb.make_benchmark("j2d5pt")
     g = eb.Grid(eb.random_grid((10, 10), seed=5).cells, "skip-update")
