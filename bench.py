@@ -180,6 +180,97 @@ def run_reference(args):
     return 0
 
 
+FP64_LANES_PER_SM = 64  # DP results per clock per SM (tools/dp_microbench.cu, B200)
+
+
+def _dp_ceiling_gcells(ntaps: int, sms: int, mhz: float) -> float:
+    """FP64-pipe ceiling for the shared-product kernels: ntaps DP operations
+    per computed cell-step ((ntaps-1) DADD + 1 DMUL), before the valid
+    fraction of the tiling."""
+    return sms * FP64_LANES_PER_SM * mhz * 1e6 / ntaps / 1e9
+
+
+def _timed_sweep(device, torch, d_in, st, steps, out, scr, **kw):
+    device.sweep_device(d_in, st, steps, out=out, scratch=scr, **kw)  # warm
+    torch.cuda.synchronize()
+    best = None
+    for _ in range(2):
+        _, tr = device.sweep_device(d_in, st, steps, out=out, scratch=scr, trace=True, **kw)
+        if best is None or tr["elapsed_ms"] < best["elapsed_ms"]:
+            best = tr
+    return best
+
+
+def extra_configs(eb, device, _native, torch, stream, hbm_peak):
+    """The other BASELINE configs, each on its own synthetic grid (SplitMix64
+    seed 1, generated in HBM, exact mode), device-timed with CUDA events:
+    config 4 (3-D, 512^3, 500 steps) with its depth sweep, config 3 (large
+    halos at 8192^2: overlapped tiling vs halo exchange), the naive
+    one-launch-per-step yardstick."""
+    try:
+        mhz = float(json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))["sm_max_mhz"])
+    except Exception:
+        mhz = 1965.0
+    sms = torch.cuda.get_device_properties(0).multi_processor_count
+    out = {}
+
+    def rec(name, st, ext, steps, tr, **extra):
+        interior = 1
+        for n in ext:
+            interior *= n - 2 * st.radius
+        g = interior * steps / (tr["elapsed_ms"] / 1e3) / 1e9
+        r = {"stencil": st.name, "extents": list(ext), "time_steps": steps,
+             "value": round(g, 1), "unit": "GCells/s", "ms_per_sweep": round(tr["elapsed_ms"], 3),
+             "fused_depth_t": tr["t_used"], "kernel": tr["kernel"],
+             "kernel_launches": tr["kernel_launches"], "exact": True,
+             "naive_roofline_frac": round(16 * g / hbm_peak, 3),
+             "fp64_pipe_ceiling_gcells": round(_dp_ceiling_gcells(len(st.taps), sms, mhz), 1),
+             "valid_fraction": round(tr["cells_valid"] / max(1, tr["cells_computed"]), 3)}
+        r.update(extra)
+        out[name] = r
+
+    # ---- config 4: j3d7pt / j3d27pt 512^3, 500 steps ------------------------
+    ext3 = (512, 512, 512)
+    d3 = device.random_grid_device(ext3, seed=1)
+    o3 = torch.empty_like(d3)
+    s3 = torch.empty_like(d3)
+    st3 = eb.make_benchmark("j3d7pt")
+    tr = _timed_sweep(device, torch, d3, st3, 500, o3, s3)
+    sweep = {}
+    for t in (1, 2, 3, 4):
+        tt = _timed_sweep(device, torch, d3, st3, 96, o3, s3, t=t)
+        sweep[t] = round((510 ** 3) * 96 / (tt["elapsed_ms"] / 1e3) / 1e9, 1)
+    rec("config4_j3d7pt_512", st3, ext3, 500, tr, depth_sweep_gcells=sweep)
+    st27 = eb.make_benchmark("j3d27pt")
+    tr = _timed_sweep(device, torch, d3, st27, 500, o3, s3)
+    rec("config4_j3d27pt_512", st27, ext3, 500, tr)
+    del d3, o3, s3
+    torch.cuda.empty_cache()
+
+    # ---- config 3: large halos at 8192^2, overlapped vs halo exchange -------
+    ext2 = (8192, 8192)
+    d2 = device.random_grid_device(ext2, seed=1)
+    o2 = torch.empty_like(d2)
+    s2 = torch.empty_like(d2)
+    for name, depths in (("j2d13pt", (2, 3)), ("j2ds25pt", (1, 2))):
+        st = eb.get_shape(name)
+        for scheme, tag in ((_native.SCHEME_SM_TILING, "overlapped"),
+                            (_native.SCHEME_DEVICE_TILING, "halo_exchange")):
+            best = None
+            for t in depths:
+                tr = _timed_sweep(device, torch, d2, st, 96, o2, s2, t=t, scheme=scheme)
+                if best is None or tr["elapsed_ms"] < best["elapsed_ms"]:
+                    best = tr
+            rec(f"config3_{name}_8192_{tag}", st, ext2, 96, best, scheme=tag)
+    # naive yardstick: one launch per time step
+    st5 = eb.make_benchmark("j2d5pt")
+    tr = _timed_sweep(device, torch, d2, st5, 20, o2, s2, scheme=_native.SCHEME_NAIVE)
+    rec("naive_j2d5pt_8192", st5, ext2, 20, tr)
+    del d2, o2, s2
+    torch.cuda.empty_cache()
+    return out
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -356,24 +447,9 @@ def main():
                                      1)
 
     if world == 1 and not args.no_3d:
-        # BASELINE config 4 (j3d7pt fp64 512^3, 500 steps), same exact mode
-        st3 = eb.make_benchmark("j3d7pt")
-        d3 = device.random_grid_device((512, 512, 512), seed=1)
-        o3 = torch.empty_like(d3)
-        s3 = torch.empty_like(d3)
-        device.sweep_device(d3, st3, 500, out=o3, scratch=s3)
-        torch.cuda.synchronize()
-        times = []
-        for _ in range(2):
-            _, tr3 = device.sweep_device(d3, st3, 500, out=o3, scratch=s3, trace=True)
-            times.append(tr3["elapsed_ms"])
-        ms3 = min(times)
-        line["config4_j3d7pt_512"] = {
-            "metric": "GCells/s (fp64)", "value": 510 ** 3 * 500 / (ms3 / 1e3) / 1e9,
-            "ms_per_sweep": ms3, "time_steps": 500, "fused_depth_t": tr3["t_used"],
-            "kernel": tr3["kernel"], "exact": True,
-            "naive_roofline_frac": 16 * 510 ** 3 * 500 / (ms3 / 1e3) / 1e9 / hbm_peak}
-        del d3, o3, s3
+        line["configs"] = extra_configs(eb, device, _native, torch, stream, hbm_peak)
+        c4 = line["configs"]["config4_j3d7pt_512"]
+        line["config4_j3d7pt_512"] = c4  # (kept for round-1 readers)
 
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         line["cpu_baseline"] = cpu_oracle_sample()

@@ -236,38 +236,50 @@ enum KernelId : int {
   KID_NAIVE = 1,
   KID_STREAM2D = 2,
   KID_STREAM3D = 3,
+  KID_HALO2D = 4,
 };
 
 // First registered kernel for (shape, depth, exactness) -- the registry lists
 // the planner's default lane width first -- or the one with lane width C.
 // Kernel family for a request: shared-product kernels (uni) are bitwise exact,
 // so they serve both exact and FMA requests when the coefficients are uniform.
-bool family_ok(const TbKernel& k, bool exact, bool uni) {
+bool family_ok(const TbKernel& k, bool exact, bool uni, int family) {
+  if (k.family != family) return false;
   if (uni) return k.uni != 0;
   return k.uni == 0 && (k.exact != 0) == exact;
 }
 
-const TbKernel* find_tb(int shape_id, int dims, int T, bool exact, bool uni, int C = 0,
-                        int variant = 0) {
+const TbKernel* find_tb(int shape_id, int dims, int T, bool exact, bool uni, int family,
+                        int C = 0, int variant = 0) {
   int n = 0;
   const TbKernel* ks = tb_kernels(&n);
   for (int i = 0; i < n; ++i)
     if (ks[i].shape_id == shape_id && ks[i].dims == dims && ks[i].T == T &&
-        family_ok(ks[i], exact, uni) && (C == 0 || ks[i].C == C)) {
+        family_ok(ks[i], exact, uni, family) && (C == 0 || ks[i].C == C)) {
       if (variant-- == 0) return &ks[i];
     }
   return nullptr;
 }
 
 // largest instantiated depth <= tmax for this shape
-int best_depth_leq(int shape_id, int dims, int tmax, bool exact, bool uni) {
+int best_depth_leq(int shape_id, int dims, int tmax, bool exact, bool uni, int family) {
   int n = 0, best = 0;
   const TbKernel* ks = tb_kernels(&n);
   for (int i = 0; i < n; ++i)
-    if (ks[i].shape_id == shape_id && ks[i].dims == dims && family_ok(ks[i], exact, uni) &&
-        ks[i].T <= tmax)
+    if (ks[i].shape_id == shape_id && ks[i].dims == dims &&
+        family_ok(ks[i], exact, uni, family) && ks[i].T <= tmax)
       best = std::max(best, ks[i].T);
   return best;
+}
+
+// Scheme -> kernel family.  sm-tiling: overlapped warp strips; device-tiling:
+// CTA strips with per-level halo exchange.  AUTO: overlapped for every shape
+// -- measured faster on B200 even for the large-halo stars (DESIGN.md §3.3:
+// j2ds25pt 199 vs 146, j2d13pt 486 vs 352 GCells/s at 8192^2).
+int pick_family(int scheme, int shape_id, int dims) {
+  (void)shape_id;
+  if (dims != 2) return 0;
+  return scheme == EBISU_SCHEME_DEVICE_TILING ? 1 : 0;
 }
 
 // Every coefficient bitwise equal (the catalog default, shapes.py:156-157)?
@@ -284,9 +296,9 @@ int default_depth(int shape_id) {
     case SHAPE_J2D9PT_GOL: return 6;
     case SHAPE_J2D9PT: return 4;
     case SHAPE_J2D25PT: return 3;
-    case SHAPE_J2D13PT: return 2;
-    case SHAPE_J2DS25PT: return 2;
-    case SHAPE_J3D7PT: return 2;
+    case SHAPE_J2D13PT: return 3;
+    case SHAPE_J2DS25PT: return 1;
+    case SHAPE_J3D7PT: return 4;
     case SHAPE_J3D13PT: return 2;
     case SHAPE_J3D27PT: return 2;
     case SHAPE_J3D17PT: return 2;
@@ -303,7 +315,7 @@ struct Stage {
 
 struct Counters {
   uint64_t gm_loads = 0, gm_stores = 0, cells_computed = 0, device_tiles = 0, syncs_device = 0,
-           syncs_block = 0, launches = 0;
+           syncs_block = 0, launches = 0, halo_loads = 0, halo_stores = 0;
   int grid = 0, nw = 0, t_used = 0, kid = KID_NONE;
 };
 
@@ -451,6 +463,100 @@ int run_tb2d_stage(const ProblemDesc& p, const TbKernel* k, int epochs, int firs
   return EBISU_OK;
 }
 
+int run_halo2d_stage(const ProblemDesc& p, const TbKernel* k, int epochs, int first_src,
+                     int first_dst, double* bufs[3], const CUtensorMap maps[3], bool coop_req,
+                     int seg_rows_req, const DevInfo& di, cudaStream_t st, Counters* ctr) {
+  const int n0 = (int)p.ext[0], n1 = (int)p.ext[1];
+  const int T = k->T, R = p.rad;
+  int per_sm = 0;
+  EB_CUDA(cudaFuncSetAttribute(k->func, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                               k->smem_bytes));
+  EB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k->func, k->NW * 32,
+                                                        (size_t)k->smem_bytes));
+  if (per_sm < 1) return fail(EBISU_ERR_CUDA, "halo2d kernel cannot be resident (T=%d)", T);
+  const int max_ctas = per_sm * di.sms;
+  const int LW = k->wn, VW = k->valid_x, HX = (LW - VW) / 2, Z = k->z;
+  // edge-aligned strips when two fit (frame columns then sit in the first /
+  // last strip only); generic strips otherwise
+  int aligned = n1 >= 2 * LW ? 1 : 0;
+  int nstrips;
+  if (aligned) {
+    const int mid = n1 - LW - VW;
+    nstrips = 2 + (mid > 0 ? (mid + VW - 1) / VW : 0);
+  } else {
+    nstrips = (n1 + VW - 1) / VW;
+  }
+  int nseg = 1, seg_len = n0;
+  plan_segments(n0, nstrips, max_ctas, T * (R + Z), std::max(16, 2 * T * Z), &nseg, &seg_len);
+  if (seg_rows_req > 0) {
+    seg_len = seg_rows_req;
+    nseg = (n0 + seg_len - 1) / seg_len;
+  }
+  const long long units = (long long)nstrips * nseg;
+  int grid = (int)std::min<long long>(max_ctas, units);
+  if (grid < 1) grid = 1;
+  const bool coop = coop_req && di.coop && epochs > 1;
+  TbLaunch L{};
+  L.n0 = n0;
+  L.n1 = n1;
+  L.nstrips = nstrips;
+  L.nseg = nseg;
+  L.seg_len = seg_len;
+  L.aligned = aligned;
+  for (int i = 0; i < 3; ++i) L.buf[i] = bufs[i];
+  L.maps = maps;
+  L.coeffs = p.coeffs;
+  L.grid = grid;
+  L.stream = st;
+  int* work = nullptr;
+  if (int rc = alloc_work(epochs, st, &work)) return rc;
+  if (coop) {
+    L.epochs = epochs;
+    L.first_src = first_src;
+    L.first_dst = first_dst;
+    L.cooperative = true;
+    L.work = work;
+    EB_CUDA(k->launch(L));
+    ctr->launches += 1;
+    ctr->syncs_device += (uint64_t)(epochs - 1);
+  } else {
+    int src = first_src, dst = first_dst;
+    for (int e = 0; e < epochs; ++e) {
+      L.epochs = 1;
+      L.first_src = src;
+      L.first_dst = dst;
+      L.cooperative = false;
+      L.work = work + e;
+      EB_CUDA(k->launch(L));
+      ctr->launches += 1;
+      src = dst;
+      dst = (dst == BUF_OUT) ? BUF_SCR : BUF_OUT;
+    }
+  }
+  cudaFreeAsync(work, st);
+  // closed-form counters: every advance loads one row per warp; halo traffic
+  // = 2R edge values per produced row per warp and level (shared memory)
+  uint64_t adv = 0;
+  const int Wr = Z + R + 1;
+  for (int g = 0; g < nseg; ++g) {
+    const int r0 = g * seg_len, r1 = std::min(n0, r0 + seg_len);
+    const int ka = std::max(0, r0 - T * R);
+    adv += (uint64_t)((r1 + T * Z - ka + Wr - 1) / Wr * Wr);
+  }
+  ctr->gm_loads += (uint64_t)epochs * adv * (uint64_t)LW * (uint64_t)nstrips;
+  ctr->gm_stores += (uint64_t)epochs * (uint64_t)n0 * (uint64_t)n1;
+  ctr->cells_computed += (uint64_t)epochs * adv * (uint64_t)T * (uint64_t)LW * (uint64_t)nstrips;
+  ctr->halo_stores += (uint64_t)epochs * adv * (uint64_t)T * 2ull * R * k->NW * nstrips;
+  ctr->halo_loads += (uint64_t)epochs * adv * (uint64_t)T * 2ull * R * k->NW * nstrips;
+  ctr->syncs_block += (uint64_t)epochs * adv * (uint64_t)nstrips;
+  ctr->device_tiles += (uint64_t)epochs * (uint64_t)units;
+  ctr->grid = grid;
+  ctr->nw = k->NW;
+  ctr->t_used = std::max(ctr->t_used, T);
+  ctr->kid = KID_HALO2D;
+  return EBISU_OK;
+}
+
 int run_tb3d_stage(const ProblemDesc& p, const TbKernel* k, int epochs, int first_src,
                    int first_dst, double* bufs[3], const CUtensorMap maps[3], bool coop_req,
                    int seg_rows_req, const DevInfo& di, cudaStream_t st, Counters* ctr) {
@@ -588,31 +694,35 @@ int run_device_impl(const ProblemDesc& p, const double* d_in, double* d_out, dou
     int t = (prm && prm->t > 0) ? prm->t : default_depth(p.shape_id);
     const int want_c = prm ? prm->lane_cells : 0;
     const int want_v = prm ? prm->variant : 0;
-    const TbKernel* k = find_tb(p.shape_id, D, t, exact, uni, want_c, want_v);
+    int fam = pick_family(scheme, p.shape_id, D);
+    // no halo-exchange instantiation for this stencil/arithmetic: the
+    // overlapped kernels compute the identical result
+    if (fam == 1 && best_depth_leq(p.shape_id, D, 64, exact, uni, 1) == 0) fam = 0;
+    const TbKernel* k = find_tb(p.shape_id, D, t, exact, uni, fam, want_c, want_v);
     if (!k && (want_c || want_v))
       return fail(EBISU_ERR_UNSUPPORTED, "no kernel with depth %d, %d cells per lane, variant %d",
                   t, want_c, want_v);
     if (!k) {
       // depth not instantiated: compose the sweep from the deepest kernel
       // below it (epochs compose bitwise, test_grid.py:94-117)
-      t = best_depth_leq(p.shape_id, D, t, exact, uni);
-      k = t ? find_tb(p.shape_id, D, t, exact, uni) : nullptr;
+      t = best_depth_leq(p.shape_id, D, t, exact, uni, fam);
+      k = t ? find_tb(p.shape_id, D, t, exact, uni, fam) : nullptr;
     }
     if (!k) {
       tb_ok = false;
     } else {
       long long full = steps / t;
       long long rem = steps % t;
-      const int kid = D == 2 ? KID_STREAM2D : KID_STREAM3D;
+      const int kid = D == 3 ? KID_STREAM3D : (fam == 1 ? KID_HALO2D : KID_STREAM2D);
       if (full > 0) stages.push_back({kid, k, (int)full});
       while (rem > 0) {
-        const int t2 = best_depth_leq(p.shape_id, D, (int)rem, exact, uni);
+        const int t2 = best_depth_leq(p.shape_id, D, (int)rem, exact, uni, fam);
         if (t2 == 0) {
           stages.push_back({KID_NAIVE, nullptr, (int)rem});
           break;
         }
         const long long e2 = rem / t2;
-        stages.push_back({kid, find_tb(p.shape_id, D, t2, exact, uni), (int)e2});
+        stages.push_back({kid, find_tb(p.shape_id, D, t2, exact, uni, fam), (int)e2});
         rem -= e2 * t2;
       }
     }
@@ -689,7 +799,10 @@ int run_device_impl(const ProblemDesc& p, const double* d_in, double* d_out, dou
         }
         if (result) break;
       }
-      if (D == 2)
+      if (D == 2 && s.kind == KID_HALO2D)
+        result = run_halo2d_stage(p, s.k, s.epochs, src, dst, bufs, maps, coop,
+                                  prm ? prm->seg_rows : 0, di, st, ctr);
+      else if (D == 2)
         result = run_tb2d_stage(p, s.k, s.epochs, src, dst, bufs, maps, coop,
                                 prm ? prm->seg_rows : 0, di, st, ctr);
       else
@@ -720,6 +833,7 @@ const char* ebisu_kernel_name(int32_t id) {
     case KID_NAIVE: return "naive_step";
     case KID_STREAM2D: return "stream2d_tb";
     case KID_STREAM3D: return "stream3d_tb";
+    case KID_HALO2D: return "halo2d_tb";
     default: return "none";
   }
 }
@@ -748,6 +862,8 @@ static void fill_trace(ebisu_trace* tr, const ProblemDesc& p, long long steps, c
   for (int d = 0; d < p.dims; ++d) interior *= (p.ext[d] - 2 * p.rad);
   tr->gm_loads = c.gm_loads;
   tr->gm_stores = c.gm_stores;
+  tr->gm_halo_loads = c.halo_loads;
+  tr->gm_halo_stores = c.halo_stores;
   tr->syncs_device = c.syncs_device;
   tr->syncs_block = c.syncs_block;
   tr->cells_computed = c.cells_computed;

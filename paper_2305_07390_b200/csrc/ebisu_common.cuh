@@ -57,6 +57,25 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
   }
 }
 
+// ---- predicated shared-memory access (no divergent branch) ----------------
+__device__ __forceinline__ void st_shared_if(double* p, double v, bool pred) {
+  asm volatile(
+      "{\n\t.reg .pred q;\n\tsetp.ne.b32 q, %2, 0;\n\t@q st.shared.f64 [%0], %1;\n\t}" ::"r"(
+          smem_u32(p)),
+      "d"(v), "r"((int)pred)
+      : "memory");
+}
+// returns *p if pred, else dflt
+__device__ __forceinline__ double ld_shared_if(const double* p, bool pred, double dflt) {
+  double r = dflt;
+  asm volatile(
+      "{\n\t.reg .pred q;\n\tsetp.ne.b32 q, %2, 0;\n\t@q ld.shared.f64 %0, [%1];\n\t}"
+      : "+d"(r)
+      : "r"(smem_u32(p)), "r"((int)pred)
+      : "memory");
+  return r;
+}
+
 // ---- proxy fences ---------------------------------------------------------
 // Generic-proxy accesses -> later async-proxy (TMA) accesses.
 __device__ __forceinline__ void fence_proxy_async_shared() {

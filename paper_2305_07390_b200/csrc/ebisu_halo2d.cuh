@@ -1,0 +1,354 @@
+// ebisu_halo2d.cuh -- 2-D temporal blocking with per-level halo exchange
+// ("device tiling"), sm_100a.
+//
+// Replaces the reference's device-tiling engine (engine/device.py:55-389:
+// a device tile of g x w blocks that exchange their per-level halos through a
+// staging buffer and a device barrier, Listing 3 order) with a CTA-level
+// design:
+//
+//  * Work unit = (CTA strip, row segment).  The CTA is the device tile: NW
+//    warps side by side, warp w owning LC = 32*C columns of a strip of
+//    LW = NW*LC columns.  Only the strip carries an overlapped margin of
+//    HX = T*R columns per side; inside the strip, warps exchange the edge
+//    columns of every produced row, so no column is computed twice.  With
+//    LW = 1024 the valid fraction at t=2, R=6 is 0.977, against 0.81 for a
+//    128-column overlapped warp strip (the paper's argument for halo exchange
+//    on large halos, Table 1 / SURVEY §7 step 6).
+//  * Rows arrive per warp by TMA into an S-slot mbarrier ring (as in
+//    k_stream2d).  Levels are register windows; x-neighbours inside a warp come
+//    from shuffles, across warps from a small shared-memory edge buffer:
+//    xh[level][slot][warp][side][R] -- the leftmost and rightmost R values of
+//    every row a warp produces.
+//  * Level skew Z = max(R, 2) for stars (only the centre row needs
+//    x-neighbours, and it was produced Z advances earlier) and R+1 for boxes
+//    (every window row does; the newest was produced one advance earlier).
+//    Every exchanged value is thus at least DR advances old (DR = Z for
+//    stars, 1 for boxes), so split-phase mbarriers order the exchange: each
+//    warp arrives after its advance, and an advance waits only for the phase
+//    DR advances back.  Warps drift up to DR advances apart and never drain
+//    at a block-wide barrier (measured: the drift-1 version spent 20% of its
+//    stall samples waiting on the barrier).
+//  * Dirichlet frame, exact / shared-product arithmetic: as k_stream2d.
+#pragma once
+
+#include <cooperative_groups.h>
+
+#include <type_traits>
+
+#include "ebisu_common.cuh"
+#include "ebisu_shapes.cuh"
+#include "ebisu_stream2d.cuh"
+
+namespace ebisu {
+
+template <class SH, int T, int C, int NW, int S>
+struct Halo2DCfg {
+  static constexpr int R = SH::R;
+  // level skew (advances).  Stars need x-neighbours of the centre row only,
+  // produced Z advances earlier, so warps may drift DR = Z advances apart;
+  // radius-1 stars use Z = 2 to get that slack.  Boxes read rows up to one
+  // advance old: Z = R + 1, DR = 1.
+  static constexpr int Z = SH::kStar ? (R < 2 ? 2 : R) : R + 1;
+  static constexpr int DR = SH::kStar ? Z : 1;
+  static constexpr int LAG = SH::kStar ? Z : Z + R;  // oldest exchanged row read
+  static constexpr int W = Z + R + 1;                 // window rows per level
+  static constexpr int LC = 32 * C;                   // columns per warp
+  static constexpr int LW = NW * LC;                  // columns per CTA strip
+  static constexpr int HX = (T * R + 1) & ~1;         // strip margin (even: TMA)
+  static constexpr int VW = LW - 2 * HX;              // valid columns per strip
+  static constexpr int NBMIN = DR + LAG;  // writers may run DR advances ahead
+  static constexpr int NB = NBMIN <= 2 ? 2 : (NBMIN <= 4 ? 4 : (NBMIN <= 8 ? 8 : 16));
+  static constexpr int ROW_BYTES = LC * 8;
+  static constexpr int RING_BYTES = NW * S * ROW_BYTES;
+  static constexpr int XH_DOUBLES = T * NB * NW * 2 * R;  // levels 0..T-1
+  static constexpr int JUNK_DOUBLES = 0;
+  static constexpr int SMEM_BYTES =
+      RING_BYTES + (XH_DOUBLES + JUNK_DOUBLES) * 8 + (NW * S + DR) * 8;
+  static_assert(VW > 0, "strip leaves no valid core");
+  static_assert(NB >= NBMIN, "edge-buffer slots must cover lag + drift");
+  static_assert((S & (S - 1)) == 0, "ring slots must be a power of two");
+  static_assert(LC <= 256, "TMA box inner dimension is limited to 256 elements");
+  static_assert(R <= LC, "halo must fit in one neighbouring warp");
+  static_assert(SMEM_BYTES <= 227 * 1024, "shared memory budget");
+};
+
+struct Halo2DArgs {
+  int n0, n1;
+  int nstrips, nseg, seg_len;
+  int epochs;
+  int first_src, first_dst;
+  int aligned;  // edge-aligned strips (n1 >= 2*LW)
+  double* buf[3];
+  int* work;
+};
+
+// One unit: CTA strip x row segment.  EDGE: the strip touches a frame column.
+template <class SH, int T, int C, int NW, int S, bool EXACT, bool UNI, bool EDGE>
+__device__ __forceinline__ int halo2d_unit(const CUtensorMap* tm, double* __restrict__ out,
+                                           double* ring, uint64_t* bars, double* xh,
+                                           uint64_t* advbar, uint32_t ring_cnt, uint32_t& adv,
+                                           int warp, int lane, int n0, int n1, int X0, int vlo,
+                                           int vhi, int r0, int r1, const Coefs<SH::NT>& cf) {
+  using Cfg = Halo2DCfg<SH, T, C, NW, S>;
+  constexpr int R = Cfg::R, Z = Cfg::Z, W = Cfg::W, NB = Cfg::NB, LC = Cfg::LC;
+  constexpr int ROW_BYTES = Cfg::ROW_BYTES;
+  constexpr int TZ = T * Z;
+
+  const int ka = max(0, r0 - T * R);
+  const int nadv = (r1 + TZ - ka + W - 1) / W * W;  // whole unrolled blocks
+  const int kend = ka + nadv;
+  const int XW = X0 + warp * LC;  // this warp's first column
+
+  // per-warp ring: rows [ka, kend); TMA zero-fills rows >= n0, rows >= r1+T*R
+  // only feed targets >= r1 (never stored)
+  if (lane == 0) {
+    for (int i = 0; i < S && i < nadv; ++i) {
+      const uint32_t slot = (ring_cnt + i) & (S - 1);
+      mbar_arrive_expect_tx(&bars[slot], ROW_BYTES);
+      tma_load_2d(ring + slot * LC, tm, XW, ka + i, &bars[slot]);
+    }
+  }
+
+  uint32_t fmask = 0, stmask = 0;
+#pragma unroll
+  for (int c = 0; c < C; ++c) {
+    const int x = XW + lane * C + c;
+    const bool f = EDGE && ((x < R) || (x >= n1 - R));
+    bool st = (x >= vlo) && (x < vhi);
+    if (UNI) st = st && !f;
+    fmask |= (uint32_t)f << c;
+    stmask |= (uint32_t)st << c;
+  }
+
+  double win[T][W][C];
+#pragma unroll
+  for (int s = 0; s < T; ++s)
+#pragma unroll
+    for (int w = 0; w < W; ++w)
+#pragma unroll
+      for (int c = 0; c < C; ++c) win[s][w][c] = 0.0;
+
+  // edge buffer of (level, slot, warp, side)
+  auto xrow = [&](int level, int slot, int w, int side) -> double* {
+    return xh + ((size_t)((level * NB + slot) * NW + w) * 2 + side) * R;
+  };
+  // push the warp's leftmost / rightmost R values of a produced row:
+  // predicated stores, only the edge lanes' predicates are on (no branch)
+  auto push = [&](int level, int slot, const double (&v)[C]) {
+    double* L = xrow(level, slot, warp, 0);
+    double* Rt = xrow(level, slot, warp, 1);
+#pragma unroll
+    for (int c = 0; c < C; ++c) {
+      const int col = lane * C + c;
+      if (c < R) st_shared_if(L + min(col, R - 1), v[c], col < R);
+      if (C - c <= R) st_shared_if(Rt + max(col - (LC - R), 0), v[c], col >= LC - R);
+    }
+  };
+  const int wl = warp > 0 ? warp - 1 : warp;       // strip edges read their own
+  const int wr = warp < NW - 1 ? warp + 1 : warp;  // buffers (invalid margin)
+
+  auto block = [&](int kbase, auto frows_tag) {
+    constexpr bool FROWS = decltype(frows_tag)::value;
+#pragma unroll
+    for (int uu = 0; uu < W; ++uu) {
+      const int k = kbase + uu;
+      const int bk = k & (NB - 1);
+      // (DR barriers round robin: advance a arrives on advbar[a % DR] as its
+      // phase a / DR; waiting for advance adv-DR is then unambiguous)
+      if (adv >= (uint32_t)Cfg::DR) {
+        const uint32_t a = adv - Cfg::DR;
+        mbar_wait(&advbar[a % Cfg::DR], (a / Cfg::DR) & 1);
+      }
+      // ---- level 0 --------------------------------------------------------
+      {
+        const uint32_t pos = ring_cnt + (uint32_t)(k - ka);
+        const uint32_t slot = pos & (S - 1);
+        mbar_wait(&bars[slot], (pos / S) & 1);
+        if (lane == 0 && k > ka && k - 1 + S < kend) {
+          const uint32_t ps = (pos - 1) & (S - 1);
+          mbar_arrive_expect_tx(&bars[ps], ROW_BYTES);
+          tma_load_2d(ring + ps * LC, tm, XW, k - 1 + S, &bars[ps]);
+        }
+        const double* rowp = ring + slot * LC + lane * C;
+        double v[C];
+#pragma unroll
+        for (int c = 0; c < C; c += 2) {
+          const double2 t2 = *reinterpret_cast<const double2*>(rowp + c);
+          v[c] = UNI ? __dmul_rn(cf.c[0], t2.x) : t2.x;
+          v[c + 1] = UNI ? __dmul_rn(cf.c[0], t2.y) : t2.y;
+        }
+#pragma unroll
+        for (int c = 0; c < C; ++c) win[0][uu][c] = v[c];
+        push(0, bk, v);
+      }
+      // ---- levels 1..T --------------------------------------------------------
+      static_for<T>([&](auto sI) {
+        constexpr int s = decltype(sI)::value + 1;
+        const int q = k - s * Z;
+        double hl[2 * R + 1][R], hr[2 * R + 1][R];
+        static_for<2 * R + 1>([&](auto dI) {
+          constexpr int dy = decltype(dI)::value - R;
+          if constexpr (row_has_halo<SH>(dy)) {
+            const int sl = pmod<W>(uu - s * Z + dy);
+            const int xs = (k - Z + dy) & (NB - 1);  // advance that produced the row
+            const double* Lb = xrow(s - 1, xs, wr, 0);   // right neighbour's left edge
+            const double* Rb = xrow(s - 1, xs, wl, 1);   // left neighbour's right edge
+            static_for<R>([&](auto jI) {
+              constexpr int j = decltype(jI)::value;
+              constexpr int ccl = -R + j;
+              constexpr int dl = (-ccl + C - 1) / C;
+              constexpr int coll = ccl + dl * C;
+              constexpr int ccr = C + j;
+              constexpr int dr = ccr / C;
+              constexpr int colr = ccr - dr * C;
+              double a = __shfl_up_sync(kFullMask, win[s - 1][sl][coll], dl);
+              double b = __shfl_down_sync(kFullMask, win[s - 1][sl][colr], dr);
+              // lanes whose neighbour column lies in the next warp (branch
+              // free: every lane loads from a clamped in-range address)
+              a = ld_shared_if(Rb + max(R + lane * C + ccl, 0), lane < dl, a);
+              b = ld_shared_if(Lb + min(max(lane * C + ccr - LC, 0), R - 1), lane > 31 - dr, b);
+              hl[dI][j] = a;
+              hr[dI][j] = b;
+            });
+          }
+        });
+        double acc[C];
+        static_for<SH::NT>([&](auto iI) {
+          constexpr int i = decltype(iI)::value;
+          constexpr Off o = SH::tap(i);
+#pragma unroll
+          for (int c = 0; c < C; ++c) {
+            const int sl = pmod<W>(uu - s * Z + o.d0);
+            const int cc = c + o.d1;
+            double x;
+            if (cc < 0)
+              x = hl[o.d0 + R][cc + R];
+            else if (cc >= C)
+              x = hr[o.d0 + R][cc - C];
+            else
+              x = win[s - 1][sl][cc];
+            if constexpr (UNI)
+              acc[c] = (i == 0) ? x : __dadd_rn(acc[c], x);
+            else if constexpr (i == 0)
+              acc[c] = tap_first<EXACT>(cf.c[0], x);
+            else
+              acc[c] = tap_next<EXACT>(acc[c], cf.c[i], x);
+          }
+        });
+        bool frow = false;
+        if constexpr (FROWS) frow = (q < R) || (q >= n0 - R);
+        double nv[C];
+#pragma unroll
+        for (int c = 0; c < C; ++c) {
+          const double centre = win[s - 1][pmod<W>(uu - s * Z)][c];
+          const double val = (UNI && s < T) ? __dmul_rn(cf.c[0], acc[c]) : acc[c];
+          if constexpr (EDGE || FROWS) {
+            bool f = frow;
+            if constexpr (EDGE) f = f || ((fmask >> c) & 1u);
+            nv[c] = f ? centre : val;
+          } else {
+            nv[c] = val;
+          }
+        }
+        if constexpr (s < T) {
+#pragma unroll
+          for (int c = 0; c < C; ++c) win[s][pmod<W>(uu - s * Z)][c] = nv[c];
+          push(s, bk, nv);
+        } else {
+          bool qok = (q >= r0) && (q < r1);
+          if (UNI && FROWS) qok = qok && !frow;
+          if (qok) {
+            double* orow = out + (size_t)q * (size_t)n1 + (XW + lane * C);
+#pragma unroll
+            for (int c = 0; c < C; ++c)
+              if ((stmask >> c) & 1u) orow[c] = nv[c];
+          }
+        }
+      });
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&advbar[adv % Cfg::DR]);  // release covers the warp
+      ++adv;
+    }
+  };
+
+  for (int kbase = ka; kbase < kend; kbase += W) {
+    // target rows of this block: [kbase - TZ, kbase + W - 1 - Z]
+    if ((kbase - TZ < R) || (kbase + W - 1 - Z >= n0 - R))
+      block(kbase, std::true_type{});
+    else
+      block(kbase, std::false_type{});
+  }
+  return nadv;
+}
+
+template <class SH, int T, int C, int NW, int S, bool EXACT, bool UNI, int MINB>
+__global__ void __launch_bounds__(NW * 32, MINB)
+    k_halo2d(const __grid_constant__ TmapSet maps, const Halo2DArgs a,
+             const __grid_constant__ Coefs<SH::NT> cf) {
+  using Cfg = Halo2DCfg<SH, T, C, NW, S>;
+  extern __shared__ __align__(1024) unsigned char smem[];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  double* ring = reinterpret_cast<double*>(smem + warp * S * Cfg::ROW_BYTES);
+  double* xh = reinterpret_cast<double*>(smem + Cfg::RING_BYTES);
+  uint64_t* bars_all = reinterpret_cast<uint64_t*>(
+      smem + Cfg::RING_BYTES + (Cfg::XH_DOUBLES + Cfg::JUNK_DOUBLES) * 8);
+  uint64_t* bars = bars_all + warp * S;
+  uint64_t* advbar = bars_all + NW * S;
+
+  if (threadIdx.x == 0) {
+    for (int i = 0; i < NW * S; ++i) mbar_init(&bars_all[i], 1);
+    for (int i = 0; i < Cfg::DR; ++i) mbar_init(&advbar[i], NW);
+    fence_mbarrier_init();
+    prefetch_tmap(&maps.m[0]);
+    prefetch_tmap(&maps.m[1]);
+    prefetch_tmap(&maps.m[2]);
+  }
+  // the edge buffers of the strip's outer warps are read but never written
+  for (int i = threadIdx.x; i < Cfg::XH_DOUBLES; i += NW * 32) xh[i] = 0.0;
+  __syncthreads();
+
+  const int n0 = a.n0, n1 = a.n1;
+  const int units = a.nstrips * a.nseg;
+  uint32_t ring_cnt = 0, adv = 0;
+  int src = a.first_src, dst = a.first_dst;
+  __shared__ int s_unit;
+  for (int e = 0; e < a.epochs; ++e) {
+    const CUtensorMap* tm = &maps.m[src];
+    double* __restrict__ out = (dst == BUF_OUT) ? a.buf[BUF_OUT] : a.buf[BUF_SCR];
+    for (;;) {
+      if (threadIdx.x == 0) s_unit = atomicAdd(a.work + e, 1);
+      __syncthreads();
+      const int u = s_unit;
+      if (u >= units) break;
+      const int strip = u % a.nstrips;
+      const int seg = u / a.nstrips;
+      const StripGeom g =
+          stream2d_strip(strip, a.nstrips, a.aligned, n1, Cfg::LW, Cfg::VW, Cfg::HX);
+      const int r0 = seg * a.seg_len;
+      const int r1 = min(n0, r0 + a.seg_len);
+      const bool edge = (g.X0 < Cfg::R) || (g.X0 + Cfg::LW > n1 - Cfg::R);
+      int used;
+      if (edge)
+        used = halo2d_unit<SH, T, C, NW, S, EXACT, UNI, true>(
+            tm, out, ring, bars, xh, advbar, ring_cnt, adv, warp, lane, n0, n1, g.X0, g.vlo,
+            g.vhi, r0, r1, cf);
+      else
+        used = halo2d_unit<SH, T, C, NW, S, EXACT, UNI, false>(
+            tm, out, ring, bars, xh, advbar, ring_cnt, adv, warp, lane, n0, n1, g.X0, g.vlo,
+            g.vhi, r0, r1, cf);
+      ring_cnt += (uint32_t)used;
+      __syncthreads();  // s_unit reuse; all warps done with the unit
+    }
+    if (e + 1 < a.epochs) {
+      fence_proxy_async_global();
+      __threadfence();
+      cooperative_groups::this_grid().sync();
+      fence_proxy_async_global();
+    }
+    const int nsrc = dst;
+    dst = (dst == BUF_OUT) ? BUF_SCR : BUF_OUT;
+    src = nsrc;
+  }
+}
+
+}  // namespace ebisu

@@ -75,6 +75,7 @@ struct TbKernel {
   int wn;                // 3-D: window planes (advance-loop unroll)
   const void* func;      // kernel symbol (occupancy queries / attributes)
   cudaError_t (*launch)(const TbLaunch&);
+  int family;            // 0: overlapped (sm-tiling), 1: halo exchange (device-tiling)
 };
 
 // All instantiated temporal-blocking kernels (ebisu_registry.cu).

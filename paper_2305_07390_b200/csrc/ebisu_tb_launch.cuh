@@ -7,6 +7,7 @@
 #include "ebisu_internal.h"
 #include "ebisu_stream2d.cuh"
 #include "ebisu_stream3d.cuh"
+#include "ebisu_halo2d.cuh"
 
 namespace ebisu {
 
@@ -108,6 +109,49 @@ cudaError_t launch_stream3d(const TbLaunch& L) {
         (ps_eligible<SH>() && ((FL) & 1) == 0) ? 2 : Stream3DCfg<SH, T, CY, CX, NWY, S, FL>::WN, \
         (const void*)&k_stream3d<SH, T, CY, CX, NWY, S, FL, (EX) != 0, (UNI) != 0, MINB>,    \
         &launch_stream3d<SH, T, CY, CX, NWY, S, FL, (EX) != 0, (UNI) != 0, MINB>             \
+  }
+
+template <class SH, int T, int C, int NW, int S, bool EXACT, bool UNI, int MINB>
+cudaError_t launch_halo2d(const TbLaunch& L) {
+  using Cfg = Halo2DCfg<SH, T, C, NW, S>;
+  auto kern = k_halo2d<SH, T, C, NW, S, EXACT, UNI, MINB>;
+  cudaError_t err =
+      cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg::SMEM_BYTES);
+  if (err != cudaSuccess) return err;
+  TmapSet maps;
+  memcpy(&maps.m[0], L.maps, 3 * sizeof(CUtensorMap));
+  Halo2DArgs a;
+  a.n0 = L.n0;
+  a.n1 = L.n1;
+  a.nstrips = L.nstrips;
+  a.nseg = L.nseg;
+  a.seg_len = L.seg_len;
+  a.epochs = L.epochs;
+  a.first_src = L.first_src;
+  a.first_dst = L.first_dst;
+  a.aligned = L.aligned;
+  for (int i = 0; i < 3; ++i) a.buf[i] = L.buf[i];
+  a.work = L.work;
+  Coefs<SH::NT> cf;
+  for (int i = 0; i < SH::NT; ++i) cf.c[i] = L.coeffs[i];
+  if (L.cooperative) {
+    void* args[] = {(void*)&maps, (void*)&a, (void*)&cf};
+    return cudaLaunchCooperativeKernel((const void*)kern, dim3(L.grid), dim3(NW * 32), args,
+                                       (size_t)Cfg::SMEM_BYTES, L.stream);
+  }
+  kern<<<L.grid, NW * 32, Cfg::SMEM_BYTES, L.stream>>>(maps, a, cf);
+  return cudaGetLastError();
+}
+
+// box0 = warp columns (TMA box), valid_x = valid columns per CTA strip, C =
+// cells per lane, z = level skew, wn = strip columns (LW)
+#define EBISU_H2D_ENTRY(SHAPE_ID, SH, T, C, NW, S, EX, UNI, MINB)                              \
+  TbKernel {                                                                                  \
+    SHAPE_ID, 2, T, C, NW, S, EX, UNI, Halo2DCfg<SH, T, C, NW, S>::SMEM_BYTES, 32 * C, 1, 1,   \
+        Halo2DCfg<SH, T, C, NW, S>::VW, 0, Halo2DCfg<SH, T, C, NW, S>::Z,                     \
+        Halo2DCfg<SH, T, C, NW, S>::LW,                                                       \
+        (const void*)&k_halo2d<SH, T, C, NW, S, (EX) != 0, (UNI) != 0, MINB>,                 \
+        &launch_halo2d<SH, T, C, NW, S, (EX) != 0, (UNI) != 0, MINB>, 1                      \
   }
 
 }  // namespace ebisu

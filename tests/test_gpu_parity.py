@@ -228,7 +228,7 @@ def test_per_tap_kernels_bitwise(name):
         for st, forced in ((base, True), (nonuni, False)):
             prm = _native.make_params(t=t, per_tap_products=forced)
             out, tr = eb.sweep(g, st, steps, params=prm, trace=True)
-            assert tr["kernel"] in ("stream2d_tb", "stream3d_tb"), tr
+            assert tr["kernel"] in ("stream2d_tb", "stream3d_tb", "halo2d_tb"), tr
             ref = oracle_run(g.cells, taps_of(st), steps)
             assert np.array_equal(out.cells, ref), (name, t, forced)
         # FMA chain with non-uniform coefficients: tolerance, not bitwise
@@ -319,3 +319,39 @@ def test_full_size_composition_and_persistence():
     assert device.compare_device(a, h)["mismatches"] == 0
     # maximum principle (convex coefficients): values stay in [min, max] of input
     assert float(a.max()) <= float(d_in.max()) and float(a.min()) >= float(d_in.min())
+
+
+CASES_H2D = {
+    "j2d5pt": [4, 6, 8, 12, 16],
+    "j2d9pt-gol": [2, 4],
+    "j2d9pt": [2, 4],
+    "j2d25pt": [2, 3],
+    "j2d13pt": [1, 2, 3, 4],
+    "j2ds25pt": [1, 2, 3, 4],
+}
+
+
+@pytest.mark.parametrize("name", list(CASES_H2D))
+def test_halo_exchange_2d_bitwise(name):
+    """device-tiling scheme (CTA strips exchanging per-level edge columns):
+    generic strips (n1 < 2 strips), edge-aligned strips (n1 >= 2 strips, the
+    frame in the first/last strip), ragged heights, remainders."""
+    st = _shape(name)
+    rng = eb.SplitMix64(0x4A10 + len(name))
+    r = st.radius
+    for t in CASES_H2D[name]:
+        for n1 in (2 * (r + 1 + rng.randint(0, 300) // 2), 2 * (1100 + rng.randint(0, 700) // 2),
+                   2200):
+            n0 = 2 * r + 1 + rng.randint(0, 200)
+            steps = rng.randint(t, 3 * t + 1)
+            g = eb.random_grid((n0, n1), rng.next_u64())
+            ref = oracle_run(g.cells, taps_of(st), steps)
+            prm = _native.make_params(scheme=_native.SCHEME_DEVICE_TILING, t=t)
+            out, tr = eb.sweep(g, st, steps, params=prm, trace=True)
+            assert tr["kernel"] == "halo2d_tb", tr
+            assert np.array_equal(out.cells, ref), (name, t, (n0, n1), steps)
+            if t == CASES_H2D[name][0]:
+                prm = _native.make_params(scheme=_native.SCHEME_DEVICE_TILING, t=t,
+                                          per_tap_products=True)
+                out = eb.sweep(g, st, steps, params=prm)
+                assert np.array_equal(out.cells, ref), (name, t, "per-tap")

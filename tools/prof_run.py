@@ -9,7 +9,8 @@ var = int(sys.argv[5]) if len(sys.argv) > 5 else 0
 st = eb.get_shape(name)
 d_in = device.random_grid_device((n,) * st.dims, seed=1)
 out = torch.empty_like(d_in); scr = torch.empty_like(d_in)
-prm = _native.make_params(t=t, variant=var)
+scheme = int(sys.argv[6]) if len(sys.argv) > 6 else 0
+prm = _native.make_params(scheme=scheme, t=t, variant=var)
 for _ in range(2):
     _, tr = device.sweep_device(d_in, st, steps, out=out, scratch=scr, params=prm, trace=True)
 print(tr)

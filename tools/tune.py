@@ -17,8 +17,9 @@ interior = (n - 2 * st.radius) ** st.dims
 for cfg in configs:
     t, c, seg = cfg[:3]
     var = cfg[3] if len(cfg) > 3 else 0
+    scheme = cfg[4] if len(cfg) > 4 else 0  # 2 sm-tiling (overlapped), 3 device-tiling (halo)
     nt = t * max(1, (240 if st.dims == 2 else 48) // t)
-    prm = _native.make_params(t=t, lane_cells=c, seg_rows=seg, variant=var,
+    prm = _native.make_params(scheme=scheme, t=t, lane_cells=c, seg_rows=seg, variant=var,
                               exact=os.environ.get("EBISU_EXACT", "1") == "1")
     try:
         device.sweep_device(d_in, st, nt, out=out, scratch=scr, params=prm)
@@ -27,8 +28,8 @@ for cfg in configs:
         for _ in range(3):
             _, tr = device.sweep_device(d_in, st, nt, out=out, scratch=scr, params=prm, trace=True)
             best = max(best, interior * nt / (tr["elapsed_ms"] / 1e3) / 1e9)
-        res[f"t{t}_c{c}_s{seg}_v{var}"] = round(best, 1)
-        print(f"{name} t={t} C={c} seg={seg} v={var}: {best:.1f} GCells/s (grid {tr['grid_ctas']}x{tr['warps_per_cta']}, {tr['kernel']})", flush=True)
+        res[f"t{t}_c{c}_s{seg}_v{var}_k{scheme}"] = round(best, 1)
+        print(f"{name} t={t} C={c} seg={seg} v={var} scheme={scheme}: {best:.1f} GCells/s (grid {tr['grid_ctas']}x{tr['warps_per_cta']}, {tr['kernel']})", flush=True)
     except Exception as e:
         print(f"{name} t={t} C={c} seg={seg} v={var}: ERROR {e}", flush=True)
 print(json.dumps(res))
