@@ -569,8 +569,19 @@ int run_tb3d_stage(const ProblemDesc& p, const TbKernel* k, int epochs, int firs
                                                         (size_t)k->smem_bytes));
   if (per_sm < 1) return fail(EBISU_ERR_CUDA, "stream3d kernel cannot be resident (T=%d)", T);
   const int max_ctas = per_sm * di.sms;
-  const int ntx = (n2 + k->valid_x - 1) / k->valid_x;
-  const int nty = (n1 + k->valid_y - 1) / k->valid_y;
+  // edge-aligned tiles when two fit along an axis (stream2d_strip geometry)
+  auto tiles_along = [](int n, int L, int V, int* aligned) {
+    if (n >= 2 * L) {
+      *aligned = 1;
+      const int mid = n - L - V;
+      return 2 + (mid > 0 ? (mid + V - 1) / V : 0);
+    }
+    *aligned = 0;
+    return (n + V - 1) / V;
+  };
+  int aligned_x = 0, aligned_y = 0;
+  const int ntx = tiles_along(n2, k->box0, k->valid_x, &aligned_x);
+  const int nty = tiles_along(n1, k->box1, k->valid_y, &aligned_y);
   const long long tiles = (long long)ntx * nty;
   int nseg = 1, seg_len = n0;
   plan_segments(n0, tiles, max_ctas, 3 * T * R, std::max(8, 2 * T * R), &nseg, &seg_len);
@@ -582,7 +593,8 @@ int run_tb3d_stage(const ProblemDesc& p, const TbKernel* k, int epochs, int firs
     // Guided schedule: start with the balanced length and halve it once the
     // remaining work is under two rounds of units, so the epoch tail (the
     // grid.sync wait) is made of short units.
-    const int min_len = std::max(8, 2 * T * R);
+    // (never below 4x the per-unit warm-up, which short segments pay in full)
+    const int min_len = std::max(std::max(8, 2 * T * R), 4 * (T * R + T * k->z));
     int cur = std::max(seg_len, min_len), pos = 0;
     while (pos < n0) {
       const long long rem = n0 - pos;
@@ -609,6 +621,8 @@ int run_tb3d_stage(const ProblemDesc& p, const TbKernel* k, int epochs, int firs
   L.n2 = n2;
   L.ntx = ntx;
   L.nty = nty;
+  L.aligned_x = aligned_x;
+  L.aligned_y = aligned_y;
   L.nseg = nseg;
   L.seg_len = seg_len;
   L.seg_start = seg_start.data();

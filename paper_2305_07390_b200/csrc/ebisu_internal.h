@@ -45,6 +45,7 @@ struct TbLaunch {
   int nstrips, nseg, seg_len;  // 2-D decomposition
   int aligned;                 // 2-D: edge-aligned strips
   int ntx, nty;                // 3-D decomposition (tiles along axis 2 / axis 1)
+  int aligned_x, aligned_y;    // 3-D: edge-aligned tiles along axis 2 / axis 1
   const int* seg_start;        // 3-D: nseg+1 segment bounds along axis 0 (guided)
   int epochs;
   int first_src, first_dst;

@@ -28,12 +28,14 @@
 
 #include "ebisu_common.cuh"
 #include "ebisu_shapes.cuh"
+#include "ebisu_stream2d.cuh"  // StripGeom / stream2d_strip (tile geometry)
 
 namespace ebisu {
 
 struct Stream3DArgs {
   int n0, n1, n2;   // extents; plane pitch n1*n2, row pitch n2
   int nty, ntx;     // tiles along axis 1 / axis 2
+  int aligned_y, aligned_x;  // edge-aligned tiles along axis 1 / axis 2
   int nseg;         // z segments
   int seg_len;      // (planner's nominal length; the real bounds are seg_start)
   // z segment j covers planes [seg_start[j], seg_start[j+1]).  Guided
@@ -123,11 +125,12 @@ template <class SH, int T, int CY, int CX, int NWY, int S, int FL, bool EXACT, b
 __device__ __forceinline__ int stream3d_unit(const CUtensorMap* tm, double* __restrict__ out,
                                              double* ring, double* halo, uint64_t* bars,
                                              uint32_t ring_cnt, int warp, int lane, int n0,
-                                             int n1, int n2, int X0, int Y0, int r0, int r1,
+                                             int n1, int n2, int X0, int Y0, int xlo, int xhi,
+                                             int ylo, int yhi, int r0, int r1,
                                              const Coefs<SH::NT>& cf) {
   using Cfg = Stream3DCfg<SH, T, CY, CX, NWY, S, FL>;
   constexpr int R = Cfg::R, Z = Cfg::Z, WN = Cfg::WN, NB = Cfg::NB;
-  constexpr int LY = Cfg::LY, LX = Cfg::LX, HY = Cfg::HY, HX = Cfg::HX;
+  constexpr int LY = Cfg::LY, LX = Cfg::LX;
   constexpr int PLANE_BYTES = LY * LX * 8;
   constexpr int TZ = T * Z;  // pipeline depth along z
   static_assert(CY * CX <= 32, "cell masks are 32-bit");
@@ -155,8 +158,7 @@ __device__ __forceinline__ int stream3d_unit(const CUtensorMap* tm, double* __re
     for (int cx = 0; cx < CX; ++cx) {
       const int yy = Y0 + ty0 + cy, xx = X0 + tx0 + cx;
       const bool f = EDGE && ((yy < R) || (yy >= n1 - R) || (xx < R) || (xx >= n2 - R));
-      bool st = (ty0 + cy >= HY) && (ty0 + cy < LY - HY) && (tx0 + cx >= HX) &&
-                (tx0 + cx < LX - HX) && (yy < n1) && (xx < n2);
+      bool st = (yy >= ylo) && (yy < yhi) && (xx >= xlo) && (xx < xhi);
       if (UNI) st = st && !f;  // shared-product levels hold products; frame pre-copied
       fmask |= (uint32_t)f << (cy * CX + cx);
       stmask |= (uint32_t)st << (cy * CX + cx);
@@ -402,12 +404,13 @@ template <class SH, int T, int CY, int CX, int NWY, int S, int FL, bool EXACT, b
 __device__ __forceinline__ int stream3d_unit_ps(const CUtensorMap* tm, double* __restrict__ out,
                                                 double* ring, double* halo, uint64_t* bars,
                                                 uint32_t ring_cnt, int warp, int lane, int n0,
-                                                int n1, int n2, int X0, int Y0, int r0, int r1,
+                                                int n1, int n2, int X0, int Y0, int xlo,
+                                                int xhi, int ylo, int yhi, int r0, int r1,
                                                 const Coefs<SH::NT>& cf) {
   using Cfg = Stream3DCfg<SH, T, CY, CX, NWY, S, FL>;
   static_assert(ps_eligible<SH>(), "partial-sum path needs a radius-1 star in catalog order");
   constexpr int NB = Cfg::NB;
-  constexpr int LY = Cfg::LY, LX = Cfg::LX, HY = Cfg::HY, HX = Cfg::HX;
+  constexpr int LY = Cfg::LY, LX = Cfg::LX;
   constexpr int PLANE_BYTES = LY * LX * 8;
   static_assert(Cfg::Z == 1 && NB >= 2, "star skew");
   static_assert(CY * CX <= 32, "cell masks are 32-bit");
@@ -437,8 +440,7 @@ __device__ __forceinline__ int stream3d_unit_ps(const CUtensorMap* tm, double* _
     for (int cx = 0; cx < CX; ++cx) {
       const int yy = Y0 + ty0 + cy, xx = X0 + tx0 + cx;
       const bool f = EDGE && ((yy < 1) || (yy >= n1 - 1) || (xx < 1) || (xx >= n2 - 1));
-      bool st = (ty0 + cy >= HY) && (ty0 + cy < LY - HY) && (tx0 + cx >= HX) &&
-                (tx0 + cx < LX - HX) && (yy < n1) && (xx < n2);
+      bool st = (yy >= ylo) && (yy < yhi) && (xx >= xlo) && (xx < xhi);
       if (UNI) st = st && !f;
       fmask |= (uint32_t)f << (cy * CX + cx);
       stmask |= (uint32_t)st << (cy * CX + cx);
@@ -644,25 +646,29 @@ __global__ void __launch_bounds__(NWY * 32, MINB)
       const int ty = tile / a.ntx;
       const int r0 = a.seg_start[j];
       const int r1 = a.seg_start[j + 1];
-      const int X0 = tx * Cfg::VX - Cfg::HX;
-      const int Y0 = ty * Cfg::VY - Cfg::HY;
+      // edge-aligned tiles (a.aligned_x/y): the first tile starts at the
+      // domain edge and the last ends there -- the frame needs no halo, so
+      // those tiles keep the margin on one side only (fewer tiles per axis)
+      const StripGeom gx = stream2d_strip(tx, a.ntx, a.aligned_x, n2, Cfg::LX, Cfg::VX, Cfg::HX);
+      const StripGeom gy = stream2d_strip(ty, a.nty, a.aligned_y, n1, Cfg::LY, Cfg::VY, Cfg::HY);
+      const int X0 = gx.X0, Y0 = gy.X0;
       const int TR = T * R;
-      const bool edge = (ty * Cfg::VY - TR < R) || ((ty + 1) * Cfg::VY + TR > n1 - R) ||
-                        (tx * Cfg::VX - TR < R) || ((tx + 1) * Cfg::VX + TR > n2 - R);
+      (void)TR;
+      const bool edge = (X0 < R) || (X0 + Cfg::LX > n2 - R) || (Y0 < R) || (Y0 + Cfg::LY > n1 - R);
       int used;
       if constexpr (ps_eligible<SH>() && (FL & 1) == 0) {
         if (edge)
           used = stream3d_unit_ps<SH, T, CY, CX, NWY, S, FL, EXACT, UNI, true>(
-              tm, out, ring, halo, bars, ring_cnt, warp, lane, n0, n1, n2, X0, Y0, r0, r1, cf);
+              tm, out, ring, halo, bars, ring_cnt, warp, lane, n0, n1, n2, X0, Y0, gx.vlo, gx.vhi, gy.vlo, gy.vhi, r0, r1, cf);
         else
           used = stream3d_unit_ps<SH, T, CY, CX, NWY, S, FL, EXACT, UNI, false>(
-              tm, out, ring, halo, bars, ring_cnt, warp, lane, n0, n1, n2, X0, Y0, r0, r1, cf);
+              tm, out, ring, halo, bars, ring_cnt, warp, lane, n0, n1, n2, X0, Y0, gx.vlo, gx.vhi, gy.vlo, gy.vhi, r0, r1, cf);
       } else if (edge)
         used = stream3d_unit<SH, T, CY, CX, NWY, S, FL, EXACT, UNI, true>(
-            tm, out, ring, halo, bars, ring_cnt, warp, lane, n0, n1, n2, X0, Y0, r0, r1, cf);
+            tm, out, ring, halo, bars, ring_cnt, warp, lane, n0, n1, n2, X0, Y0, gx.vlo, gx.vhi, gy.vlo, gy.vhi, r0, r1, cf);
       else
         used = stream3d_unit<SH, T, CY, CX, NWY, S, FL, EXACT, UNI, false>(
-            tm, out, ring, halo, bars, ring_cnt, warp, lane, n0, n1, n2, X0, Y0, r0, r1, cf);
+            tm, out, ring, halo, bars, ring_cnt, warp, lane, n0, n1, n2, X0, Y0, gx.vlo, gx.vhi, gy.vlo, gy.vhi, r0, r1, cf);
       ring_cnt += (uint32_t)used;
       __syncthreads();  // halo buffers and s_unit are reused by the next unit
     }

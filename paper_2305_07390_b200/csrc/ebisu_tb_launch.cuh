@@ -80,6 +80,8 @@ cudaError_t launch_stream3d(const TbLaunch& L) {
   a.n2 = L.n2;
   a.nty = L.nty;
   a.ntx = L.ntx;
+  a.aligned_x = L.aligned_x;
+  a.aligned_y = L.aligned_y;
   a.nseg = L.nseg;
   a.seg_len = L.seg_len;
   if (L.nseg > EBISU_MAX_SEGS) return cudaErrorInvalidValue;
