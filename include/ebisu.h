@@ -93,7 +93,10 @@ typedef struct ebisu_params {
   int32_t seg_rows;          /* rows per work unit along axis 0 (0 = planner)       */
   int32_t variant;           /* n-th registered kernel for (shape, t) (0 = default) */
   int32_t per_tap_products;  /* 1: never share products between taps (see below)   */
-  int32_t reserved[2];
+  int32_t out_planes[2];     /* write only output planes [lo, hi) along axis 0; {0,0}
+                                = all.  Needs a single fused epoch (steps <= t): the
+                                multi-GPU driver computes its boundary band first,
+                                sends it, and computes the interior while NCCL runs */
 } ebisu_params;
 /* Shared products: when every coefficient of the stencil is bitwise equal (the
  * catalog default 1/|taps|, shapes.py:148-157), term_k = RN(c*x_k) depends on

@@ -75,7 +75,7 @@ class ParamsC(ctypes.Structure):
         ("seg_rows", ctypes.c_int32),
         ("variant", ctypes.c_int32),
         ("per_tap_products", ctypes.c_int32),
-        ("reserved", ctypes.c_int32 * 2),
+        ("out_planes", ctypes.c_int32 * 2),
     ]
 
 
@@ -193,7 +193,7 @@ def make_params(scheme: int = SCHEME_AUTO, t: int = 0, tile=(0, 0), device_tile_
                 lazy: bool = False, exact: bool = True, persistent: bool = True,
                 validate_tile: bool = False, lane_cells: int = 0,
                 seg_rows: int = 0, variant: int = 0,
-                per_tap_products: bool = False) -> ParamsC:
+                per_tap_products: bool = False, out_planes=(0, 0)) -> ParamsC:
     p = ParamsC()
     p.scheme = scheme
     p.t = int(t)
@@ -209,6 +209,7 @@ def make_params(scheme: int = SCHEME_AUTO, t: int = 0, tile=(0, 0), device_tile_
     p.seg_rows = int(seg_rows)
     p.variant = int(variant)
     p.per_tap_products = int(bool(per_tap_products))
+    p.out_planes[0], p.out_planes[1] = int(out_planes[0]), int(out_planes[1])
     return p
 
 

@@ -120,6 +120,11 @@ int validate(const ebisu_stencil* st, int ndim, const int64_t* ext, const ebisu_
     if (prm->scheme < EBISU_SCHEME_AUTO || prm->scheme > EBISU_SCHEME_DEVICE_TILING)
       return fail(EBISU_ERR_PARAM, "unknown scheme %d", prm->scheme);
     if (prm->t < 0) return fail(EBISU_ERR_PARAM, "temporal depth must be >= 1");
+    if (prm->out_planes[1] != 0 &&
+        (prm->out_planes[0] < 0 || prm->out_planes[0] >= prm->out_planes[1] ||
+         prm->out_planes[1] > ext[0]))
+      return fail(EBISU_ERR_PARAM, "output-plane range [%d, %d) outside [0, %lld)",
+                  prm->out_planes[0], prm->out_planes[1], (long long)ext[0]);
     if (prm->validate_tile && prm->t >= 1) {
       // engine/params.py:52-90 (reference TilingParams.validate)
       const int t = prm->t;
@@ -372,11 +377,12 @@ int run_tb2d_stage(const ProblemDesc& p, const TbKernel* k, int epochs, int firs
   const int LC = k->box0, HX = (LC - VW) / 2;
   int aligned = 0;
   const int nstrips = stream2d_nstrips(n1, LC, VW, HX, R, k->C, &aligned);
-  int nseg = 1, seg_len = n0;
-  plan_segments(n0, nstrips, total_warps, 2 * T * R, std::max(16, 2 * T * R), &nseg, &seg_len);
+  const int span = p.z_hi - p.z_lo;  // output rows of this call
+  int nseg = 1, seg_len = span;
+  plan_segments(span, nstrips, total_warps, 2 * T * R, std::max(16, 2 * T * R), &nseg, &seg_len);
   if (seg_rows_req > 0) {
     seg_len = seg_rows_req;
-    nseg = (n0 + seg_len - 1) / seg_len;
+    nseg = (span + seg_len - 1) / seg_len;
   }
   const long long units = (long long)nstrips * nseg;
   // every resident warp pulls units dynamically
@@ -390,6 +396,8 @@ int run_tb2d_stage(const ProblemDesc& p, const TbKernel* k, int epochs, int firs
   L.nstrips = nstrips;
   L.nseg = nseg;
   L.seg_len = seg_len;
+  L.z_lo = p.z_lo;
+  L.z_hi = p.z_hi;
   L.first_src = first_src;
   L.first_dst = first_dst;
   L.aligned = aligned;
@@ -446,13 +454,13 @@ int run_tb2d_stage(const ProblemDesc& p, const TbKernel* k, int epochs, int firs
   // closed-form counters (reference ExecutionTrace semantics, trace.py:1-17)
   uint64_t loads = 0, adv = 0;
   for (int g = 0; g < nseg; ++g) {
-    const int r0 = g * seg_len, r1 = std::min(n0, r0 + seg_len);
+    const int r0 = p.z_lo + g * seg_len, r1 = std::min(p.z_hi, r0 + seg_len);
     const int ka = std::max(0, r0 - T * R), kb = std::min(n0, r1 + T * R);
     loads += (uint64_t)(kb - ka);
     adv += (uint64_t)(r1 + T * R - ka);
   }
   ctr->gm_loads += (uint64_t)epochs * loads * (uint64_t)(32 * k->C) * (uint64_t)nstrips;
-  ctr->gm_stores += (uint64_t)epochs * (uint64_t)n0 * (uint64_t)n1;
+  ctr->gm_stores += (uint64_t)epochs * (uint64_t)span * (uint64_t)n1;
   ctr->cells_computed +=
       (uint64_t)epochs * adv * (uint64_t)T * (uint64_t)(32 * k->C) * (uint64_t)nstrips;
   ctr->device_tiles += (uint64_t)epochs * (uint64_t)units;
@@ -486,11 +494,12 @@ int run_halo2d_stage(const ProblemDesc& p, const TbKernel* k, int epochs, int fi
   } else {
     nstrips = (n1 + VW - 1) / VW;
   }
-  int nseg = 1, seg_len = n0;
-  plan_segments(n0, nstrips, max_ctas, T * (R + Z), std::max(16, 2 * T * Z), &nseg, &seg_len);
+  const int span = p.z_hi - p.z_lo;
+  int nseg = 1, seg_len = span;
+  plan_segments(span, nstrips, max_ctas, T * (R + Z), std::max(16, 2 * T * Z), &nseg, &seg_len);
   if (seg_rows_req > 0) {
     seg_len = seg_rows_req;
-    nseg = (n0 + seg_len - 1) / seg_len;
+    nseg = (span + seg_len - 1) / seg_len;
   }
   const long long units = (long long)nstrips * nseg;
   int grid = (int)std::min<long long>(max_ctas, units);
@@ -502,6 +511,8 @@ int run_halo2d_stage(const ProblemDesc& p, const TbKernel* k, int epochs, int fi
   L.nstrips = nstrips;
   L.nseg = nseg;
   L.seg_len = seg_len;
+  L.z_lo = p.z_lo;
+  L.z_hi = p.z_hi;
   L.aligned = aligned;
   for (int i = 0; i < 3; ++i) L.buf[i] = bufs[i];
   L.maps = maps;
@@ -539,12 +550,12 @@ int run_halo2d_stage(const ProblemDesc& p, const TbKernel* k, int epochs, int fi
   uint64_t adv = 0;
   const int Wr = Z + R + 1;
   for (int g = 0; g < nseg; ++g) {
-    const int r0 = g * seg_len, r1 = std::min(n0, r0 + seg_len);
+    const int r0 = p.z_lo + g * seg_len, r1 = std::min(p.z_hi, r0 + seg_len);
     const int ka = std::max(0, r0 - T * R);
     adv += (uint64_t)((r1 + T * Z - ka + Wr - 1) / Wr * Wr);
   }
   ctr->gm_loads += (uint64_t)epochs * adv * (uint64_t)LW * (uint64_t)nstrips;
-  ctr->gm_stores += (uint64_t)epochs * (uint64_t)n0 * (uint64_t)n1;
+  ctr->gm_stores += (uint64_t)epochs * (uint64_t)span * (uint64_t)n1;
   ctr->cells_computed += (uint64_t)epochs * adv * (uint64_t)T * (uint64_t)LW * (uint64_t)nstrips;
   ctr->halo_stores += (uint64_t)epochs * adv * (uint64_t)T * 2ull * R * k->NW * nstrips;
   ctr->halo_loads += (uint64_t)epochs * adv * (uint64_t)T * 2ull * R * k->NW * nstrips;
@@ -583,21 +594,22 @@ int run_tb3d_stage(const ProblemDesc& p, const TbKernel* k, int epochs, int firs
   const int ntx = tiles_along(n2, k->box0, k->valid_x, &aligned_x);
   const int nty = tiles_along(n1, k->box1, k->valid_y, &aligned_y);
   const long long tiles = (long long)ntx * nty;
-  int nseg = 1, seg_len = n0;
-  plan_segments(n0, tiles, max_ctas, 3 * T * R, std::max(8, 2 * T * R), &nseg, &seg_len);
+  const int span = p.z_hi - p.z_lo;  // output planes of this call
+  int nseg = 1, seg_len = span;
+  plan_segments(span, tiles, max_ctas, 3 * T * R, std::max(8, 2 * T * R), &nseg, &seg_len);
   std::vector<int> seg_start;
   if (seg_rows_req > 0) {
     seg_len = seg_rows_req;
-    for (int r = 0; r < n0; r += seg_len) seg_start.push_back(r);
+    for (int r = p.z_lo; r < p.z_hi; r += seg_len) seg_start.push_back(r);
   } else {
     // Guided schedule: start with the balanced length and halve it once the
     // remaining work is under two rounds of units, so the epoch tail (the
     // grid.sync wait) is made of short units.
     // (never below 4x the per-unit warm-up, which short segments pay in full)
     const int min_len = std::max(std::max(8, 2 * T * R), 4 * (T * R + T * k->z));
-    int cur = std::max(seg_len, min_len), pos = 0;
-    while (pos < n0) {
-      const long long rem = n0 - pos;
+    int cur = std::max(seg_len, min_len), pos = p.z_lo;
+    while (pos < p.z_hi) {
+      const long long rem = p.z_hi - pos;
       while (cur > min_len && rem * tiles < 2ll * cur * max_ctas) cur = std::max(min_len, cur / 2);
       seg_start.push_back(pos);
       pos += (int)std::min<long long>(cur, rem);
@@ -605,12 +617,12 @@ int run_tb3d_stage(const ProblemDesc& p, const TbKernel* k, int epochs, int firs
   }
   if ((int)seg_start.size() > EBISU_MAX_SEGS) {
     // too fine: fall back to uniform segments within the table
-    seg_len = (n0 + EBISU_MAX_SEGS - 1) / EBISU_MAX_SEGS;
+    seg_len = (span + EBISU_MAX_SEGS - 1) / EBISU_MAX_SEGS;
     seg_start.clear();
-    for (int r = 0; r < n0; r += seg_len) seg_start.push_back(r);
+    for (int r = p.z_lo; r < p.z_hi; r += seg_len) seg_start.push_back(r);
   }
   nseg = (int)seg_start.size();
-  seg_start.push_back(n0);
+  seg_start.push_back(p.z_hi);
   const long long units = tiles * nseg;
   int grid = (int)std::min<long long>(max_ctas, units);
   if (grid < 1) grid = 1;
@@ -668,7 +680,7 @@ int run_tb3d_stage(const ProblemDesc& p, const TbKernel* k, int epochs, int firs
   }
   const uint64_t tile_cells = (uint64_t)k->box0 * (uint64_t)k->box1;
   ctr->gm_loads += (uint64_t)epochs * loads * tile_cells * (uint64_t)ntx * nty;
-  ctr->gm_stores += (uint64_t)epochs * (uint64_t)n0 * n1 * n2;
+  ctr->gm_stores += (uint64_t)epochs * (uint64_t)span * n1 * n2;
   ctr->cells_computed += (uint64_t)epochs * adv * (uint64_t)T * tile_cells * (uint64_t)ntx * nty;
   ctr->device_tiles += (uint64_t)epochs * (uint64_t)units;
   ctr->syncs_block += (uint64_t)epochs * adv * (uint64_t)ntx * nty;
@@ -679,8 +691,12 @@ int run_tb3d_stage(const ProblemDesc& p, const TbKernel* k, int epochs, int firs
   return EBISU_OK;
 }
 
-int run_device_impl(const ProblemDesc& p, const double* d_in, double* d_out, double* d_scr,
+int run_device_impl(const ProblemDesc& p0, const double* d_in, double* d_out, double* d_scr,
                     long long steps, const ebisu_params* prm, cudaStream_t st, Counters* ctr) {
+  ProblemDesc p = p0;
+  const bool ranged = prm && prm->out_planes[1] > 0;
+  p.z_lo = ranged ? prm->out_planes[0] : 0;
+  p.z_hi = ranged ? prm->out_planes[1] : (int)p.ext[0];
   DevInfo di;
   int rc = device_info(&di);
   if (rc) return rc;
@@ -749,6 +765,11 @@ int run_device_impl(const ProblemDesc& p, const double* d_in, double* d_out, dou
   // ---- buffers: every stage writes a full grid (frame included) -----------------
   long long nwrites = 0;  // number of grid writes
   for (auto& s : stages) nwrites += s.epochs;
+  if (ranged && nwrites != 1)
+    return fail(EBISU_ERR_PARAM,
+                "output-plane range needs a single fused epoch (steps <= t with a kernel of "
+                "that depth), got %lld writes",
+                nwrites);
   double* scr = d_scr;
   bool own_scr = false;
   if (nwrites > 1 && !scr) {

@@ -75,6 +75,7 @@ struct Halo2DCfg {
 struct Halo2DArgs {
   int n0, n1;
   int nstrips, nseg, seg_len;
+  int z_lo, z_hi;  // output rows [z_lo, z_hi)
   int epochs;
   int first_src, first_dst;
   int aligned;  // edge-aligned strips (n1 >= 2*LW)
@@ -324,8 +325,8 @@ __global__ void __launch_bounds__(NW * 32, MINB)
       const int seg = u / a.nstrips;
       const StripGeom g =
           stream2d_strip(strip, a.nstrips, a.aligned, n1, Cfg::LW, Cfg::VW, Cfg::HX);
-      const int r0 = seg * a.seg_len;
-      const int r1 = min(n0, r0 + a.seg_len);
+      const int r0 = a.z_lo + seg * a.seg_len;
+      const int r1 = min(a.z_hi, r0 + a.seg_len);
       const bool edge = (g.X0 < Cfg::R) || (g.X0 + Cfg::LW > n1 - Cfg::R);
       int used;
       if (edge)

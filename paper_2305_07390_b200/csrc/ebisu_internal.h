@@ -26,10 +26,11 @@ struct ProblemDesc {
   const int* offsets;    // [ntaps][dims]
   const double* coeffs;  // [ntaps]
   int shape_id;          // ShapeId or SHAPE_GENERIC
+  int z_lo = 0, z_hi = 0;  // output planes [z_lo, z_hi) along axis 0 (set by the driver)
 };
 
 cudaError_t launch_naive_step(const ProblemDesc& p, const double* in, double* out, bool exact,
-                              cudaStream_t st, int num_sms);
+                              cudaStream_t st, int num_sms);  // writes planes [z_lo, z_hi)
 cudaError_t launch_frame_copy(const ProblemDesc& p, const double* in, double* out,
                               cudaStream_t st, int num_sms);
 cudaError_t launch_splitmix(unsigned long long seed, long long start, long long n, double* out,
@@ -43,6 +44,7 @@ struct TbLaunch {
   // geometry
   int n0, n1, n2;  // extents (2-D: n2 unused)
   int nstrips, nseg, seg_len;  // 2-D decomposition
+  int z_lo, z_hi;              // output rows/planes [z_lo, z_hi) along axis 0
   int aligned;                 // 2-D: edge-aligned strips
   int ntx, nty;                // 3-D decomposition (tiles along axis 2 / axis 1)
   int aligned_x, aligned_y;    // 3-D: edge-aligned tiles along axis 2 / axis 1

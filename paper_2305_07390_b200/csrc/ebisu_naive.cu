@@ -16,6 +16,7 @@ struct NaiveTaps {
   int rad;
   int dims;
   long long n0, n1, n2;  // extents (unused axes = 1)
+  long long z_lo, z_hi;  // output planes [z_lo, z_hi) along axis 0
   long long lin[EBISU_MAX_TAPS];  // linear offsets
   double coef[EBISU_MAX_TAPS];
 };
@@ -24,10 +25,12 @@ template <bool EXACT>
 __global__ void __launch_bounds__(256) k_naive_step(const double* __restrict__ in,
                                                     double* __restrict__ out,
                                                     const __grid_constant__ NaiveTaps tp) {
-  const long long total = tp.n0 * tp.n1 * tp.n2;
+  const long long plane = tp.n1 * tp.n2;
+  const long long base = tp.z_lo * plane;
+  const long long total = (tp.z_hi - tp.z_lo) * plane;
   const long long stride = (long long)gridDim.x * blockDim.x;
-  for (long long idx = (long long)blockIdx.x * blockDim.x + threadIdx.x; idx < total;
-       idx += stride) {
+  for (long long idx = base + (long long)blockIdx.x * blockDim.x + threadIdx.x;
+       idx < base + total; idx += stride) {
     const long long i2 = idx % tp.n2;
     const long long r = idx / tp.n2;
     const long long i1 = r % tp.n1;
@@ -57,6 +60,8 @@ cudaError_t launch_naive_step(const ProblemDesc& p, const double* in, double* ou
   tp.n0 = p.ext[0];
   tp.n1 = p.dims >= 2 ? p.ext[1] : 1;
   tp.n2 = p.dims >= 3 ? p.ext[2] : 1;
+  tp.z_lo = p.z_lo;
+  tp.z_hi = p.z_hi > 0 ? p.z_hi : p.ext[0];
   for (int t = 0; t < p.ntaps; ++t) {
     const int* o = p.offsets + t * p.dims;
     long long l = o[0];
@@ -65,7 +70,7 @@ cudaError_t launch_naive_step(const ProblemDesc& p, const double* in, double* ou
     tp.lin[t] = l;
     tp.coef[t] = p.coeffs[t];
   }
-  const long long total = tp.n0 * tp.n1 * tp.n2;
+  const long long total = (tp.z_hi - tp.z_lo) * tp.n1 * tp.n2;
   long long blocks = (total + 255) / 256;
   const long long cap = (long long)num_sms * 8;
   if (blocks > cap) blocks = cap;
@@ -84,11 +89,11 @@ cudaError_t launch_naive_step(const ProblemDesc& p, const double* in, double* ou
 __global__ void __launch_bounds__(256) k_frame_copy(const double* __restrict__ in,
                                                     double* __restrict__ out, long long P,
                                                     long long Y, long long X, int R0, int R1,
-                                                    int R2) {
+                                                    int R2, long long row_lo, long long row_hi) {
   const int lane = threadIdx.x & 31;
   const long long warps = (long long)gridDim.x * (blockDim.x >> 5);
-  for (long long row = (long long)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
-       row < P * Y; row += warps) {
+  for (long long row = row_lo + (long long)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+       row < row_hi; row += warps) {
     const long long pp = row / Y, y = row % Y;
     const double* src = in + row * X;
     double* dst = out + row * X;
@@ -117,12 +122,18 @@ cudaError_t launch_frame_copy(const ProblemDesc& p, const double* in, double* ou
     X = p.ext[2];
     R0 = R1 = p.rad;
   }
-  const long long rows = P * Y;
+  // rows of the output-plane range only (axis 0 = planes in 3-D, rows in 2-D)
+  const long long z_hi = p.z_hi > 0 ? p.z_hi : p.ext[0];
+  const long long per = p.dims == 3 ? Y : 1;
+  long long row_lo = (long long)p.z_lo * per, row_hi = z_hi * per;
+  if (p.dims == 1) row_lo = 0, row_hi = 1;
+  const long long rows = row_hi - row_lo;
   long long blocks = (rows + 7) / 8;
   const long long cap = (long long)num_sms * 8;
   if (blocks > cap) blocks = cap;
   if (blocks < 1) blocks = 1;
-  k_frame_copy<<<(unsigned)blocks, 256, 0, st>>>(in, out, P, Y, X, R0, R1, p.rad);
+  k_frame_copy<<<(unsigned)blocks, 256, 0, st>>>(in, out, P, Y, X, R0, R1, p.rad, row_lo,
+                                                 row_hi);
   return cudaGetLastError();
 }
 

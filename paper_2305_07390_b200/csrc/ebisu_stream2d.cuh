@@ -52,6 +52,7 @@ struct Stream2DArgs {
   int nstrips;       // warp strips along axis 1
   int nseg;          // row segments along axis 0
   int seg_len;       // rows per segment
+  int z_lo, z_hi;    // output rows [z_lo, z_hi) (segments tile this range)
   int epochs;        // fused epochs in this launch
   int first_src;     // BufId of epoch 0's source
   int first_dst;     // BufId of epoch 0's destination
@@ -388,8 +389,8 @@ __global__ void __launch_bounds__(NW * 32, MINB)
       const int seg = u / a.nstrips;
       const StripGeom g =
           stream2d_strip(strip, a.nstrips, a.aligned, n1, Cfg::LC, Cfg::VW, Cfg::HX);
-      const int r0 = seg * a.seg_len;
-      const int r1 = min(n0, r0 + a.seg_len);
+      const int r0 = a.z_lo + seg * a.seg_len;
+      const int r1 = min(a.z_hi, r0 + a.seg_len);
       const int ka = max(0, r0 - TR);
       const int kb = min(n0, r1 + TR);
       long long t_start = 0;

@@ -38,6 +38,7 @@ struct Stream3DArgs {
   int aligned_y, aligned_x;  // edge-aligned tiles along axis 1 / axis 2
   int nseg;         // z segments
   int seg_len;      // (planner's nominal length; the real bounds are seg_start)
+  int z_lo, z_hi;   // output planes [z_lo, z_hi) (informational: seg_start tiles it)
   // z segment j covers planes [seg_start[j], seg_start[j+1]).  Guided
   // schedule: segments shrink toward the end of the list, and units are
   // handed out segment-major, so the epoch tail is made of short units.

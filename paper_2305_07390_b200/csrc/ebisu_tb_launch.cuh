@@ -26,6 +26,8 @@ cudaError_t launch_stream2d(const TbLaunch& L) {
   a.nstrips = L.nstrips;
   a.nseg = L.nseg;
   a.seg_len = L.seg_len;
+  a.z_lo = L.z_lo;
+  a.z_hi = L.z_hi;
   a.epochs = L.epochs;
   a.first_src = L.first_src;
   a.first_dst = L.first_dst;
@@ -84,6 +86,8 @@ cudaError_t launch_stream3d(const TbLaunch& L) {
   a.aligned_y = L.aligned_y;
   a.nseg = L.nseg;
   a.seg_len = L.seg_len;
+  a.z_lo = L.z_lo;
+  a.z_hi = L.z_hi;
   if (L.nseg > EBISU_MAX_SEGS) return cudaErrorInvalidValue;
   for (int j = 0; j <= L.nseg; ++j) a.seg_start[j] = L.seg_start[j];
   a.epochs = L.epochs;
@@ -128,6 +132,8 @@ cudaError_t launch_halo2d(const TbLaunch& L) {
   a.nstrips = L.nstrips;
   a.nseg = L.nseg;
   a.seg_len = L.seg_len;
+  a.z_lo = L.z_lo;
+  a.z_hi = L.z_hi;
   a.epochs = L.epochs;
   a.first_src = L.first_src;
   a.first_dst = L.first_dst;

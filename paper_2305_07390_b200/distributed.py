@@ -6,10 +6,15 @@ B200 build's scale-out of ``reference_run`` over the GPUs of one node.
 * Rank g owns the contiguous planes ``[own0, own1)`` of axis 0 (the streaming
   axis, slowest in C order, so slabs and halos are contiguous blocks).
 * Each rank keeps ``H = t*R`` ghost planes on every interior face.  Per epoch
-  (t fused steps): exchange H boundary planes with each neighbour (NCCL
-  point-to-point ``send/recv`` through ``torch.distributed``, one batched group
-  per epoch), then run the epoch on ghost+owned planes with the single-GPU
-  kernel (``ebisu_run_device``).  The array faces at ghost boundaries are
+  (t fused steps), overlapped: (1) compute the two boundary bands -- the H
+  owned planes next to each interior face, the only outputs a neighbour
+  needs -- with the single-GPU kernel restricted to those output planes
+  (``ebisu_params.out_planes``); (2) on a communication stream, send the
+  bands and receive the neighbours' bands straight into the ghost planes
+  (NCCL point-to-point through ``torch.distributed``, one batched group);
+  (3) meanwhile compute the interior planes, which need no ghost; (4) join.
+  Slabs thinner than 2H, and the remainder epoch of a step count that is not
+  a multiple of t, run unsplit and exchange afterwards.  The array faces at ghost boundaries are
   treated as frame by the kernel; the error this introduces travels R planes
   per step, so after t steps it has crossed exactly the H ghost planes and the
   owned planes are exact -- bitwise equal to ``reference_run`` on the full
@@ -71,10 +76,14 @@ def slab_plan(n0: int, world: int, rank: int, halo: int) -> SlabPlan:
 
 
 def _default_step(stencil: StencilShape, exact: bool):
-    from . import device
+    from . import _native, device
 
-    def step(src, dst, scratch, steps, t):
-        device.sweep_device(src, stencil, steps, out=dst, scratch=scratch, t=t, exact=exact)
+    def step(src, dst, scratch, steps, t, planes=None):
+        if planes is None:
+            device.sweep_device(src, stencil, steps, out=dst, scratch=scratch, t=t, exact=exact)
+        else:
+            prm = _native.make_params(t=t, exact=exact, out_planes=planes)
+            device.sweep_device(src, stencil, steps, out=dst, params=prm)
 
     return step
 
@@ -123,6 +132,8 @@ class SlabSweep:
         self.a = a
         self.b = torch.empty_like(a)
         self.scratch = torch.empty_like(a)
+        self.comm = torch.cuda.Stream(self.device) if a.is_cuda else None
+        self.overlapped_epochs = 0
 
     # -- data --------------------------------------------------------------
     def _fill_random(self, a, seed: int):
@@ -185,16 +196,73 @@ class SlabSweep:
             hi0 = p.ghost_lo + own_n
             a[hi0:hi0 + depth].copy_(recv_hi)
 
+    def _bands(self):
+        """Local plane ranges: (lower band, upper band, interior) of the owned
+        planes; a band is None on a face without neighbour."""
+        p, H = self.plan, self.halo
+        o0, o1 = p.ghost_lo, p.ghost_lo + (p.own1 - p.own0)
+        lo = (o0, o0 + H) if p.rank > 0 else None
+        hi = (o1 - H, o1) if p.rank < p.world - 1 else None
+        return lo, hi, (o0 + (H if lo else 0), o1 - (H if hi else 0))
+
+    def _exchange_bands(self, dst, lo, hi):
+        """Send the freshly computed bands of ``dst``; receive the neighbours'
+        bands straight into the ghost planes of ``dst``."""
+        dist, p, H = self.dist, self.plan, self.halo
+        ops = []
+        if lo:
+            ops.append(dist.P2POp(dist.isend, dst[lo[0]:lo[1]], p.rank - 1, self.group))
+            ops.append(dist.P2POp(dist.irecv, dst[lo[0] - H:lo[0]], p.rank - 1, self.group))
+        if hi:
+            ops.append(dist.P2POp(dist.isend, dst[hi[0]:hi[1]], p.rank + 1, self.group))
+            ops.append(dist.P2POp(dist.irecv, dst[hi[1]:hi[1] + H], p.rank + 1, self.group))
+        for w in dist.batch_isend_irecv(ops):
+            w.wait()
+
+    def _epoch_overlapped(self):
+        """One t-step epoch: bands, then exchange (comm stream) || interior."""
+        t = self.t
+        lo, hi, inner = self._bands()
+        for band in (lo, hi):
+            if band:
+                self.step(self.a, self.b, None, t, t, planes=band)
+        if self.comm is not None:
+            torch = self.torch
+            compute = torch.cuda.current_stream(self.device)
+            self.comm.wait_stream(compute)  # bands computed
+            with torch.cuda.stream(self.comm):
+                self._exchange_bands(self.b, lo, hi)
+            if inner[1] > inner[0]:
+                self.step(self.a, self.b, None, t, t, planes=inner)
+            compute.wait_stream(self.comm)  # ghosts of the next epoch landed
+        else:
+            self._exchange_bands(self.b, lo, hi)
+            if inner[1] > inner[0]:
+                self.step(self.a, self.b, None, t, t, planes=inner)
+        self.overlapped_epochs += 1
+
     # -- sweep ------------------------------------------------------------------
     def run(self, steps: int):
         """Advance the distributed grid by ``steps`` Jacobi steps."""
         if steps < 0:
             raise ValueError("step count must be >= 0")
+        if steps == 0:
+            return self.owned()
+        own_n = self.plan.own1 - self.plan.own0
+        split = self.world > 1 and own_n >= 2 * self.halo
+        self.exchange(self.halo)  # ghosts current from here on
         done = 0
         while done < steps:
             d = min(self.t, steps - done)
-            self.exchange(d * self.stencil.radius)
-            self.step(self.a, self.b, self.scratch, d, d)
+            if split and d == self.t:
+                self._epoch_overlapped()
+            else:
+                self.step(self.a, self.b, self.scratch, d, d)
+                self.a, self.b = self.b, self.a
+                if done + d < steps:
+                    self.exchange(self.halo)
+                done += d
+                continue
             self.a, self.b = self.b, self.a
             done += d
         return self.owned()

@@ -51,11 +51,20 @@ def _worker(rank, world, port, results):
             st = eb.get_shape(name)
             taps = taps_of(st)
 
-            def step(src, dst, scratch, n, _t, taps=taps):
-                dst.copy_(torch.from_numpy(reference_run(src.numpy(), taps, n)))
+            def step(src, dst, scratch, n, _t, planes=None, taps=taps):
+                # same contract as the kernel: ``planes`` restricts the planes
+                # written (ebisu_params.out_planes); the rest of dst is untouched
+                res = torch.from_numpy(reference_run(src.numpy(), taps, n))
+                if planes is None:
+                    dst.copy_(res)
+                else:
+                    dst[planes[0]:planes[1]].copy_(res[planes[0]:planes[1]])
 
             sw = SlabSweep(st, ext, t=t, seed=1000 + i, step=step, device=torch.device("cpu"))
             sw.run(steps)
+            own_n = sw.plan.own1 - sw.plan.own0
+            if own_n >= 2 * sw.halo and steps >= t:
+                assert sw.overlapped_epochs == steps // t, (name, sw.overlapped_epochs)
             full = sw.gather(0)
             if rank == 0:
                 out[i] = full.numpy()

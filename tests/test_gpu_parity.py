@@ -355,3 +355,36 @@ def test_halo_exchange_2d_bitwise(name):
                                           per_tap_products=True)
                 out = eb.sweep(g, st, steps, params=prm)
                 assert np.array_equal(out.cells, ref), (name, t, "per-tap")
+
+
+@pytest.mark.parametrize("name,ext,t,scheme", [
+    ("j2d5pt", (300, 258), 8, 0), ("j2d5pt", (300, 2200), 4, 3), ("j2ds25pt", (260, 400), 2, 0),
+    ("j3d7pt", (70, 66, 130), 4, 0), ("j3d27pt", (41, 40, 70), 2, 0), ("j3d13pt", (50, 34, 66), 1, 0),
+])
+def test_output_plane_range(name, ext, t, scheme):
+    """ebisu_params.out_planes (the multi-GPU band/interior split): two ranged
+    calls tile the full one-epoch result bitwise and nothing outside the range
+    is written."""
+    from paper_2305_07390_b200 import device
+
+    torch = _torch()
+    st = _shape(name)
+    d_in = device.random_grid_device(ext, seed=5)
+    full = torch.empty_like(d_in)
+    device.sweep_device(d_in, st, t, out=full, params=_native.make_params(t=t, scheme=scheme))
+    cut = ext[0] // 3 + 1
+    split = torch.full_like(d_in, float("nan"))
+    for lo, hi in ((cut, ext[0]), (0, cut)):
+        prm = _native.make_params(t=t, scheme=scheme, out_planes=(lo, hi))
+        device.sweep_device(d_in, st, t, out=split, params=prm)
+        if lo == cut:  # first call: nothing below the range written yet
+            assert torch.isnan(split[:cut]).all()
+    torch.cuda.synchronize()
+    assert torch.equal(split, full), (name, ext, t)
+    ref = oracle_run(d_in.cpu().numpy(), taps_of(st), t)
+    assert np.array_equal(full.cpu().numpy(), ref)
+    # a ranged call that would need several epochs is refused
+    with pytest.raises(Exception, match="single fused epoch"):
+        device.sweep_device(d_in, st, 2 * t + 1, out=split,
+                            params=_native.make_params(t=t, out_planes=(0, cut)))
+
