@@ -353,6 +353,33 @@ void plan_segments(int n0, long long tiles, long long slots, int warm, int min_l
   *nseg_out = (n0 + best_len - 1) / best_len;
 }
 
+// Guided segment list over output rows/planes [z_lo, z_hi): start with the
+// balanced length and halve it once the remaining work is under two rounds of
+// units, so the epoch tail (the grid.sync wait) is made of short units; never
+// below min_len (short segments pay the per-unit warm-up in full).
+std::vector<int> guided_segments(int z_lo, int z_hi, long long tiles, long long slots,
+                                 int seg_len, int min_len, int seg_rows_req) {
+  std::vector<int> seg_start;
+  if (seg_rows_req > 0) {
+    for (int r = z_lo; r < z_hi; r += seg_rows_req) seg_start.push_back(r);
+  } else {
+    int cur = std::max(seg_len, min_len), pos = z_lo;
+    while (pos < z_hi) {
+      const long long rem = z_hi - pos;
+      while (cur > min_len && rem * tiles < 2ll * cur * slots) cur = std::max(min_len, cur / 2);
+      seg_start.push_back(pos);
+      pos += (int)std::min<long long>(cur, rem);
+    }
+  }
+  if ((int)seg_start.size() > EBISU_MAX_SEGS) {
+    const int len = (z_hi - z_lo + EBISU_MAX_SEGS - 1) / EBISU_MAX_SEGS;
+    seg_start.clear();
+    for (int r = z_lo; r < z_hi; r += len) seg_start.push_back(r);
+  }
+  seg_start.push_back(z_hi);
+  return seg_start;
+}
+
 // Per-epoch dynamic-scheduling counters for one stage (zeroed on `st`).
 int alloc_work(int epochs, cudaStream_t st, int** out) {
   EB_CUDA(cudaMallocAsync((void**)out, sizeof(int) * (size_t)std::max(epochs, 1), st));
@@ -380,10 +407,12 @@ int run_tb2d_stage(const ProblemDesc& p, const TbKernel* k, int epochs, int firs
   const int span = p.z_hi - p.z_lo;  // output rows of this call
   int nseg = 1, seg_len = span;
   plan_segments(span, nstrips, total_warps, 2 * T * R, std::max(16, 2 * T * R), &nseg, &seg_len);
-  if (seg_rows_req > 0) {
-    seg_len = seg_rows_req;
-    nseg = (span + seg_len - 1) / seg_len;
-  }
+  // uniform segments: the guided schedule measured 3 % slower here (per-warp
+  // units are already short; the extra warm-ups cost more than the tail)
+  const std::vector<int> seg_start =
+      guided_segments(p.z_lo, p.z_hi, nstrips, total_warps, seg_len, seg_len,
+                      seg_rows_req > 0 ? seg_rows_req : seg_len);
+  nseg = (int)seg_start.size() - 1;
   const long long units = (long long)nstrips * nseg;
   // every resident warp pulls units dynamically
   int grid = (int)std::min<long long>(max_ctas, (units + k->NW - 1) / k->NW);
@@ -396,6 +425,7 @@ int run_tb2d_stage(const ProblemDesc& p, const TbKernel* k, int epochs, int firs
   L.nstrips = nstrips;
   L.nseg = nseg;
   L.seg_len = seg_len;
+  L.seg_start = seg_start.data();
   L.z_lo = p.z_lo;
   L.z_hi = p.z_hi;
   L.first_src = first_src;
@@ -454,7 +484,7 @@ int run_tb2d_stage(const ProblemDesc& p, const TbKernel* k, int epochs, int firs
   // closed-form counters (reference ExecutionTrace semantics, trace.py:1-17)
   uint64_t loads = 0, adv = 0;
   for (int g = 0; g < nseg; ++g) {
-    const int r0 = p.z_lo + g * seg_len, r1 = std::min(p.z_hi, r0 + seg_len);
+    const int r0 = seg_start[g], r1 = seg_start[g + 1];
     const int ka = std::max(0, r0 - T * R), kb = std::min(n0, r1 + T * R);
     loads += (uint64_t)(kb - ka);
     adv += (uint64_t)(r1 + T * R - ka);
@@ -597,32 +627,11 @@ int run_tb3d_stage(const ProblemDesc& p, const TbKernel* k, int epochs, int firs
   const int span = p.z_hi - p.z_lo;  // output planes of this call
   int nseg = 1, seg_len = span;
   plan_segments(span, tiles, max_ctas, 3 * T * R, std::max(8, 2 * T * R), &nseg, &seg_len);
-  std::vector<int> seg_start;
-  if (seg_rows_req > 0) {
-    seg_len = seg_rows_req;
-    for (int r = p.z_lo; r < p.z_hi; r += seg_len) seg_start.push_back(r);
-  } else {
-    // Guided schedule: start with the balanced length and halve it once the
-    // remaining work is under two rounds of units, so the epoch tail (the
-    // grid.sync wait) is made of short units.
-    // (never below 4x the per-unit warm-up, which short segments pay in full)
-    const int min_len = std::max(std::max(8, 2 * T * R), 4 * (T * R + T * k->z));
-    int cur = std::max(seg_len, min_len), pos = p.z_lo;
-    while (pos < p.z_hi) {
-      const long long rem = p.z_hi - pos;
-      while (cur > min_len && rem * tiles < 2ll * cur * max_ctas) cur = std::max(min_len, cur / 2);
-      seg_start.push_back(pos);
-      pos += (int)std::min<long long>(cur, rem);
-    }
-  }
-  if ((int)seg_start.size() > EBISU_MAX_SEGS) {
-    // too fine: fall back to uniform segments within the table
-    seg_len = (span + EBISU_MAX_SEGS - 1) / EBISU_MAX_SEGS;
-    seg_start.clear();
-    for (int r = p.z_lo; r < p.z_hi; r += seg_len) seg_start.push_back(r);
-  }
-  nseg = (int)seg_start.size();
-  seg_start.push_back(p.z_hi);
+  // (never below 4x the per-unit warm-up, which short segments pay in full)
+  const std::vector<int> seg_start = guided_segments(
+      p.z_lo, p.z_hi, tiles, max_ctas, seg_len,
+      std::max(std::max(8, 2 * T * R), 4 * (T * R + T * k->z)), seg_rows_req);
+  nseg = (int)seg_start.size() - 1;
   const long long units = tiles * nseg;
   int grid = (int)std::min<long long>(max_ctas, units);
   if (grid < 1) grid = 1;

@@ -53,6 +53,9 @@ struct Stream2DArgs {
   int nseg;          // row segments along axis 0
   int seg_len;       // rows per segment
   int z_lo, z_hi;    // output rows [z_lo, z_hi) (segments tile this range)
+  // row segment j = [seg_start[j], seg_start[j+1]); guided schedule (long
+  // segments handed out first, short ones at the epoch tail), as in 3-D
+  int seg_start[EBISU_MAX_SEGS + 1];
   int epochs;        // fused epochs in this launch
   int first_src;     // BufId of epoch 0's source
   int first_dst;     // BufId of epoch 0's destination
@@ -389,8 +392,8 @@ __global__ void __launch_bounds__(NW * 32, MINB)
       const int seg = u / a.nstrips;
       const StripGeom g =
           stream2d_strip(strip, a.nstrips, a.aligned, n1, Cfg::LC, Cfg::VW, Cfg::HX);
-      const int r0 = a.z_lo + seg * a.seg_len;
-      const int r1 = min(a.z_hi, r0 + a.seg_len);
+      const int r0 = a.seg_start[seg];
+      const int r1 = a.seg_start[seg + 1];
       const int ka = max(0, r0 - TR);
       const int kb = min(n0, r1 + TR);
       long long t_start = 0;

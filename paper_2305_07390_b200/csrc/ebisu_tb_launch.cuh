@@ -32,6 +32,8 @@ cudaError_t launch_stream2d(const TbLaunch& L) {
   a.first_src = L.first_src;
   a.first_dst = L.first_dst;
   a.aligned = L.aligned;
+  if (L.nseg > EBISU_MAX_SEGS) return cudaErrorInvalidValue;
+  for (int j = 0; j <= L.nseg; ++j) a.seg_start[j] = L.seg_start[j];
   for (int i = 0; i < 3; ++i) a.buf[i] = L.buf[i];
   a.unit_clock = L.unit_clock;
   a.work = L.work;
