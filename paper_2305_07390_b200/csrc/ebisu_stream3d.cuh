@@ -602,6 +602,229 @@ __device__ __forceinline__ int stream3d_unit_ps(const CUtensorMap* tm, double* _
   return nadv;
 }
 
+// Plane-major radius-1 stencils (j3d27pt, j3d17pt, poisson: taps sorted by
+// axis-0 offset, the catalog's lexicographic order): each plane of the level
+// below is gathered with its in-plane neighbourhood ONCE and feeds the three
+// targets it touches -- the z+1 taps of target c-1 (completing it), the z taps
+// of target c, the z-1 taps of target c+1 -- as consecutive runs of the
+// reference order.  A level keeps two partial sums, the plane it will consume
+// next and the plane it consumed last (frame carry): no 3-plane neighbourhood
+// per advance, a third of the shuffles and halo loads of the window path.
+template <class SH>
+__host__ __device__ constexpr bool pm_eligible() {
+  if (SH::dims != 3 || SH::R != 1 || SH::kStar) return false;
+  for (int i = 1; i < SH::NT; ++i)
+    if (SH::tap(i).d0 < SH::tap(i - 1).d0) return false;
+  return true;
+}
+
+template <class SH, int T, int CY, int CX, int NWY, int S, int FL, bool EXACT, bool UNI, bool EDGE>
+__device__ __forceinline__ int stream3d_unit_pm(const CUtensorMap* tm, double* __restrict__ out,
+                                                double* ring, double* halo, uint64_t* bars,
+                                                uint32_t ring_cnt, int warp, int lane, int n0,
+                                                int n1, int n2, int X0, int Y0, int xlo,
+                                                int xhi, int ylo, int yhi, int r0, int r1,
+                                                const Coefs<SH::NT>& cf) {
+  using Cfg = Stream3DCfg<SH, T, CY, CX, NWY, S, FL>;
+  static_assert(pm_eligible<SH>(), "plane-major path needs sorted radius-1 taps");
+  constexpr int NB = Cfg::NB;
+  constexpr int LY = Cfg::LY, LX = Cfg::LX;
+  constexpr int PLANE_BYTES = LY * LX * 8;
+  static_assert(NB >= 2, "halo slots");
+  static_assert(CY * CX <= 32, "cell masks are 32-bit");
+  static_assert(CX % 2 == 0, "double2 rows");
+
+  const int ka = max(0, r0 - T);
+  // level s emits plane k - 2s; advances in pairs (register sets alternate)
+  const int nadv = (r1 + 2 * T - ka + 1) & ~1;
+  const int kend = ka + nadv;
+  const int tid = warp * 32 + lane;
+  const int ty0 = warp * CY;
+  const int tx0 = lane * CX;
+
+  if (tid == 0) {
+    for (int i = 0; i < S && i < nadv; ++i) {
+      const uint32_t slot = (ring_cnt + i) & (S - 1);
+      mbar_arrive_expect_tx(&bars[slot], PLANE_BYTES);
+      tma_load_3d(ring + slot * Cfg::RING_PLANE, tm, X0, Y0, ka + i, &bars[slot]);
+    }
+  }
+
+  uint32_t fmask = 0, stmask = 0;
+#pragma unroll
+  for (int cy = 0; cy < CY; ++cy)
+#pragma unroll
+    for (int cx = 0; cx < CX; ++cx) {
+      const int yy = Y0 + ty0 + cy, xx = X0 + tx0 + cx;
+      const bool f = EDGE && ((yy < 1) || (yy >= n1 - 1) || (xx < 1) || (xx >= n2 - 1));
+      bool st = (yy >= ylo) && (yy < yhi) && (xx >= xlo) && (xx < xhi);
+      if (UNI) st = st && !f;
+      fmask |= (uint32_t)f << (cy * CX + cx);
+      stmask |= (uint32_t)st << (cy * CX + cx);
+    }
+
+  // per level s (1..T), index s-1:  A = target c+1 after its z-1 taps,
+  // B = target c after its z-1 and z taps, Yc = the level-below plane to
+  // consume next advance, Yp = the one consumed last (frame carry)
+  double A[T][CY][CX], B[T][CY][CX], Yc[T][CY][CX], Yp[T][CY][CX];
+#pragma unroll
+  for (int s = 0; s < T; ++s)
+#pragma unroll
+    for (int cy = 0; cy < CY; ++cy)
+#pragma unroll
+      for (int cx = 0; cx < CX; ++cx) A[s][cy][cx] = B[s][cy][cx] = Yc[s][cy][cx] = Yp[s][cy][cx] = 0.0;
+
+  auto hrow = [&](int level, int b, int w, int r) -> double* {
+    return halo + (size_t)(level * NB + b) * Cfg::HPLANE + (size_t)(w * 2 + r) * LX + tx0;
+  };
+  auto push = [&](int level, int b, const double (&v)[CY][CX]) {
+#pragma unroll
+    for (int r = 0; r < 2; ++r) {
+      const int cy = r == 0 ? 0 : CY - 1;
+      double* d = hrow(level, b, warp, r);
+#pragma unroll
+      for (int cx = 0; cx < CX; cx += 2)
+        *reinterpret_cast<double2*>(d + cx) = make_double2(v[cy][cx], v[cy][cx + 1]);
+    }
+  };
+  const int wa = warp > 0 ? warp - 1 : warp;
+  const int wbl = warp < NWY - 1 ? warp + 1 : warp;
+  const long long plane = (long long)n1 * (long long)n2;
+  double* obase = out + ((long long)(Y0 + ty0) * n2 + (X0 + tx0));
+
+  // sum of the taps with axis-0 offset DZ over the gathered neighbourhood,
+  // starting from `acc` (FIRST: the run opens the target's sum)
+  auto run_taps = [&](auto dz_tag, auto first_tag, const double (&e)[CY + 2][CX + 2], int cy,
+                      int cx, double acc) -> double {
+    constexpr int DZ = decltype(dz_tag)::value;
+    constexpr bool FIRST = decltype(first_tag)::value;
+    static_for<SH::NT>([&](auto iI) {
+      constexpr int i = decltype(iI)::value;
+      constexpr Off o = SH::tap(i);
+      if constexpr (o.d0 == DZ) {
+        const double x = e[cy + 1 + o.d1][cx + 1 + o.d2];
+        constexpr bool OPEN = FIRST && (i == 0 || SH::tap(i > 0 ? i - 1 : 0).d0 != DZ);
+        if constexpr (UNI)
+          acc = OPEN ? x : __dadd_rn(acc, x);
+        else if constexpr (OPEN)
+          acc = tap_first<EXACT>(cf.c[i], x);
+        else
+          acc = tap_next<EXACT>(acc, cf.c[i], x);
+      }
+    });
+    return acc;
+  };
+
+  auto advance = [&](int k, auto fpl_tag) {
+    constexpr bool FPL = decltype(fpl_tag)::value;
+    const int bk = k & (NB - 1);
+    const int bp = (k - 1) & (NB - 1);
+    double nw[CY][CX];  // newest plane of the level below (produced this advance)
+    {
+      const uint32_t pos = ring_cnt + (uint32_t)(k - ka);
+      const uint32_t slot = pos & (S - 1);
+      mbar_wait(&bars[slot], (pos / S) & 1);
+      const double* p = ring + slot * Cfg::RING_PLANE + ty0 * LX + tx0;
+#pragma unroll
+      for (int cy = 0; cy < CY; ++cy)
+#pragma unroll
+        for (int cx = 0; cx < CX; cx += 2) {
+          const double2 t2 = *reinterpret_cast<const double2*>(p + cy * LX + cx);
+          nw[cy][cx] = UNI ? __dmul_rn(cf.c[0], t2.x) : t2.x;
+          nw[cy][cx + 1] = UNI ? __dmul_rn(cf.c[0], t2.y) : t2.y;
+        }
+      push(0, bk, nw);
+    }
+    static_for<T>([&](auto sI) {
+      constexpr int s = decltype(sI)::value + 1;
+      const int q = k - 2 * s;  // target completed this advance (= consumed plane - 1)
+      bool fpl = false;
+      if constexpr (FPL) fpl = (q < 1) || (q >= n0 - 1);
+      // gather the consumed plane (level s-1, produced last advance) once
+      double e[CY + 2][CX + 2];
+#pragma unroll
+      for (int cy = 0; cy < CY; ++cy)
+#pragma unroll
+        for (int cx = 0; cx < CX; ++cx) e[cy + 1][cx + 1] = Yc[s - 1][cy][cx];
+      {
+        const double* up = hrow(s - 1, bp, wa, warp > 0 ? 1 : 0);
+        const double* dn = hrow(s - 1, bp, wbl, warp < NWY - 1 ? 0 : 1);
+#pragma unroll
+        for (int cx = 0; cx < CX; cx += 2) {
+          const double2 a2 = *reinterpret_cast<const double2*>(up + cx);
+          const double2 b2 = *reinterpret_cast<const double2*>(dn + cx);
+          e[0][cx + 1] = a2.x;
+          e[0][cx + 2] = a2.y;
+          e[CY + 1][cx + 1] = b2.x;
+          e[CY + 1][cx + 2] = b2.y;
+        }
+      }
+#pragma unroll
+      for (int ey = 0; ey < CY + 2; ++ey) {
+        e[ey][0] = __shfl_up_sync(kFullMask, e[ey][CX], 1);
+        e[ey][CX + 1] = __shfl_down_sync(kFullMask, e[ey][1], 1);
+      }
+      double nv[CY][CX];
+#pragma unroll
+      for (int cy = 0; cy < CY; ++cy)
+#pragma unroll
+        for (int cx = 0; cx < CX; ++cx) {
+          const double C = run_taps(std::integral_constant<int, 1>{}, std::false_type{}, e, cy,
+                                    cx, B[s - 1][cy][cx]);
+          const double Bn = run_taps(std::integral_constant<int, 0>{}, std::false_type{}, e,
+                                     cy, cx, A[s - 1][cy][cx]);
+          const double An = run_taps(std::integral_constant<int, -1>{}, std::true_type{}, e, cy,
+                                     cx, 0.0);
+          const double val = (UNI && s < T) ? __dmul_rn(cf.c[0], C) : C;
+          if constexpr (EDGE || FPL) {
+            bool f = fpl;
+            if constexpr (EDGE) f = f || ((fmask >> (cy * CX + cx)) & 1u);
+            nv[cy][cx] = f ? Yp[s - 1][cy][cx] : val;
+          } else {
+            nv[cy][cx] = val;
+          }
+          A[s - 1][cy][cx] = An;
+          B[s - 1][cy][cx] = Bn;
+          Yp[s - 1][cy][cx] = Yc[s - 1][cy][cx];
+          Yc[s - 1][cy][cx] = nw[cy][cx];
+          nw[cy][cx] = nv[cy][cx];
+        }
+      if constexpr (s < T) {
+        push(s, bk, nv);
+      } else {
+        bool qok = (q >= r0) && (q < r1);
+        if (UNI && FPL) qok = qok && !fpl;
+        if (qok) {
+          double* o = obase + (long long)q * plane;
+#pragma unroll
+          for (int cy = 0; cy < CY; ++cy)
+#pragma unroll
+            for (int cx = 0; cx < CX; ++cx)
+              if ((stmask >> (cy * CX + cx)) & 1u) o[(long long)cy * n2 + cx] = nv[cy][cx];
+        }
+      }
+    });
+    __syncthreads();
+    if (tid == 0 && k + S < kend) {
+      const uint32_t slot = (ring_cnt + (uint32_t)(k - ka)) & (S - 1);
+      mbar_arrive_expect_tx(&bars[slot], PLANE_BYTES);
+      tma_load_3d(ring + slot * Cfg::RING_PLANE, tm, X0, Y0, k + S, &bars[slot]);
+    }
+  };
+
+  for (int k = ka; k < kend; k += 2) {
+    // targets of these two advances: [k + 1 - 2T, k - 1]
+    if ((k + 1 - 2 * T < 1) || (k - 1 >= n0 - 1)) {
+      advance(k, std::true_type{});
+      advance(k + 1, std::true_type{});
+    } else {
+      advance(k, std::false_type{});
+      advance(k + 1, std::false_type{});
+    }
+  }
+  return nadv;
+}
+
 template <class SH, int T, int CY, int CX, int NWY, int S, int FL, bool EXACT, bool UNI, int MINB>
 __global__ void __launch_bounds__(NWY * 32, MINB)
     k_stream3d(const __grid_constant__ TmapSet maps, const Stream3DArgs a,
@@ -657,7 +880,16 @@ __global__ void __launch_bounds__(NWY * 32, MINB)
       (void)TR;
       const bool edge = (X0 < R) || (X0 + Cfg::LX > n2 - R) || (Y0 < R) || (Y0 + Cfg::LY > n1 - R);
       int used;
-      if constexpr (ps_eligible<SH>() && (FL & 1) == 0) {
+      if constexpr (pm_eligible<SH>() && (FL & 1) == 0) {
+        if (edge)
+          used = stream3d_unit_pm<SH, T, CY, CX, NWY, S, FL, EXACT, UNI, true>(
+              tm, out, ring, halo, bars, ring_cnt, warp, lane, n0, n1, n2, X0, Y0, gx.vlo, gx.vhi,
+              gy.vlo, gy.vhi, r0, r1, cf);
+        else
+          used = stream3d_unit_pm<SH, T, CY, CX, NWY, S, FL, EXACT, UNI, false>(
+              tm, out, ring, halo, bars, ring_cnt, warp, lane, n0, n1, n2, X0, Y0, gx.vlo, gx.vhi,
+              gy.vlo, gy.vhi, r0, r1, cf);
+      } else if constexpr (ps_eligible<SH>() && (FL & 1) == 0) {
         if (edge)
           used = stream3d_unit_ps<SH, T, CY, CX, NWY, S, FL, EXACT, UNI, true>(
               tm, out, ring, halo, bars, ring_cnt, warp, lane, n0, n1, n2, X0, Y0, gx.vlo, gx.vhi, gy.vlo, gy.vhi, r0, r1, cf);

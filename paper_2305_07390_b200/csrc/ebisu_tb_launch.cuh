@@ -114,7 +114,8 @@ cudaError_t launch_stream3d(const TbLaunch& L) {
         Stream3DCfg<SH, T, CY, CX, NWY, S, FL>::LX, Stream3DCfg<SH, T, CY, CX, NWY, S, FL>::LY, \
         1, Stream3DCfg<SH, T, CY, CX, NWY, S, FL>::VX,                                        \
         Stream3DCfg<SH, T, CY, CX, NWY, S, FL>::VY, Stream3DCfg<SH, T, CY, CX, NWY, S, FL>::Z,  \
-        (ps_eligible<SH>() && ((FL) & 1) == 0) ? 2 : Stream3DCfg<SH, T, CY, CX, NWY, S, FL>::WN, \
+        ((ps_eligible<SH>() || pm_eligible<SH>()) && ((FL) & 1) == 0)                        \
+            ? 2 : Stream3DCfg<SH, T, CY, CX, NWY, S, FL>::WN,                                  \
         (const void*)&k_stream3d<SH, T, CY, CX, NWY, S, FL, (EX) != 0, (UNI) != 0, MINB>,    \
         &launch_stream3d<SH, T, CY, CX, NWY, S, FL, (EX) != 0, (UNI) != 0, MINB>             \
   }
