@@ -813,8 +813,8 @@ __device__ __forceinline__ int stream3d_unit_pm(const CUtensorMap* tm, double* _
   };
 
   for (int k = ka; k < kend; k += 2) {
-    // targets of these two advances: [k + 1 - 2T, k - 1]
-    if ((k + 1 - 2 * T < 1) || (k - 1 >= n0 - 1)) {
+    // targets of these two advances: [k - 2T, k - 1]
+    if ((k - 2 * T < 1) || (k - 1 >= n0 - 1)) {
       advance(k, std::true_type{});
       advance(k + 1, std::true_type{});
     } else {
