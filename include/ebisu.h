@@ -153,6 +153,20 @@ EBISU_API int32_t ebisu_run_device(const ebisu_stencil* stencil, int32_t ndim,
                          const ebisu_params* params, void* stream,
                          ebisu_trace* trace /* nullable */);
 
+/* fp32 sweeps (north-star tolerance mode, 1e-5 relative to the fp64
+ * reference): same contract with float buffers; arithmetic in binary32 with
+ * the same operation order (coefficients rounded to float once).  The fast
+ * path needs the last extent to be a multiple of 4 (16-byte TMA rows). */
+EBISU_API int32_t ebisu_run_host_f32(const ebisu_stencil* stencil, int32_t ndim,
+                           const int64_t* extents, const float* in, float* out,
+                           int64_t steps, const ebisu_params* params,
+                           ebisu_trace* trace /* nullable */);
+EBISU_API int32_t ebisu_run_device_f32(const ebisu_stencil* stencil, int32_t ndim,
+                             const int64_t* extents, const float* d_in, float* d_out,
+                             float* d_scratch, int64_t steps,
+                             const ebisu_params* params, void* stream,
+                             ebisu_trace* trace /* nullable */);
+
 /* SplitMix64 uniforms [0,1): d_out[i] = draw i of SplitMix64(seed) for
  * i in [start, start+n). Bit-identical to rng.uniform_array. */
 EBISU_API int32_t ebisu_random_grid_device(uint64_t seed, int64_t start, int64_t n,

@@ -38,6 +38,8 @@ EXPORTS = (
     "ebisu_check_compatible",
     "ebisu_run_host",
     "ebisu_run_device",
+    "ebisu_run_host_f32",
+    "ebisu_run_device_f32",
     "ebisu_random_grid_device",
     "ebisu_compare_device",
     "ebisu_release_scratch",
@@ -142,6 +144,10 @@ def load() -> ctypes.CDLL:
         lib.ebisu_run_device.argtypes = [ctypes.POINTER(StencilC), i32, ctypes.POINTER(i64),
                                          vp, vp, vp, i64, ctypes.POINTER(ParamsC), vp,
                                          ctypes.POINTER(TraceC)]
+        lib.ebisu_run_host_f32.restype = i32
+        lib.ebisu_run_host_f32.argtypes = lib.ebisu_run_host.argtypes
+        lib.ebisu_run_device_f32.restype = i32
+        lib.ebisu_run_device_f32.argtypes = lib.ebisu_run_device.argtypes
         lib.ebisu_random_grid_device.restype = i32
         lib.ebisu_random_grid_device.argtypes = [u64, i64, i64, vp, vp]
         lib.ebisu_compare_device.restype = i32

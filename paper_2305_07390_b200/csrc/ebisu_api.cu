@@ -212,13 +212,13 @@ PFN_cuTensorMapEncodeTiled_v12000 get_encode() {
   return fn;
 }
 
-int encode_map(CUtensorMap* m, const double* base, int rank, const long long* dims_fast_first,
-               const int* box_fast_first) {
+int encode_map(CUtensorMap* m, const void* base, int rank, const long long* dims_fast_first,
+               const int* box_fast_first, int elem) {
   auto enc = get_encode();
   if (!enc) return fail(EBISU_ERR_CUDA, "cuTensorMapEncodeTiled unavailable");
   cuuint64_t gdim[3], gstride[2];
   cuuint32_t box[3], estr[3];
-  long long pitch = 8;
+  long long pitch = elem;
   for (int i = 0; i < rank; ++i) {
     gdim[i] = (cuuint64_t)dims_fast_first[i];
     box[i] = (cuuint32_t)box_fast_first[i];
@@ -228,7 +228,8 @@ int encode_map(CUtensorMap* m, const double* base, int rank, const long long* di
       gstride[i] = (cuuint64_t)pitch;
     }
   }
-  CUresult r = enc(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, (cuuint32_t)rank, (void*)base, gdim,
+  CUresult r = enc(m, elem == 4 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT32 : CU_TENSOR_MAP_DATA_TYPE_FLOAT64,
+                   (cuuint32_t)rank, const_cast<void*>(base), gdim,
                    gstride, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
                    CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   if (r != CUDA_SUCCESS) return fail(EBISU_ERR_CUDA, "cuTensorMapEncodeTiled failed (%d)", (int)r);
@@ -248,31 +249,32 @@ enum KernelId : int {
 // the planner's default lane width first -- or the one with lane width C.
 // Kernel family for a request: shared-product kernels (uni) are bitwise exact,
 // so they serve both exact and FMA requests when the coefficients are uniform.
-bool family_ok(const TbKernel& k, bool exact, bool uni, int family) {
-  if (k.family != family) return false;
+bool family_ok(const TbKernel& k, bool exact, bool uni, int family, int elem) {
+  if (k.family != family || k.elem != elem) return false;
   if (uni) return k.uni != 0;
   return k.uni == 0 && (k.exact != 0) == exact;
 }
 
 const TbKernel* find_tb(int shape_id, int dims, int T, bool exact, bool uni, int family,
-                        int C = 0, int variant = 0) {
+                        int elem, int C = 0, int variant = 0) {
   int n = 0;
   const TbKernel* ks = tb_kernels(&n);
   for (int i = 0; i < n; ++i)
     if (ks[i].shape_id == shape_id && ks[i].dims == dims && ks[i].T == T &&
-        family_ok(ks[i], exact, uni, family) && (C == 0 || ks[i].C == C)) {
+        family_ok(ks[i], exact, uni, family, elem) && (C == 0 || ks[i].C == C)) {
       if (variant-- == 0) return &ks[i];
     }
   return nullptr;
 }
 
 // largest instantiated depth <= tmax for this shape
-int best_depth_leq(int shape_id, int dims, int tmax, bool exact, bool uni, int family) {
+int best_depth_leq(int shape_id, int dims, int tmax, bool exact, bool uni, int family,
+                   int elem) {
   int n = 0, best = 0;
   const TbKernel* ks = tb_kernels(&n);
   for (int i = 0; i < n; ++i)
     if (ks[i].shape_id == shape_id && ks[i].dims == dims &&
-        family_ok(ks[i], exact, uni, family) && ks[i].T <= tmax)
+        family_ok(ks[i], exact, uni, family, elem) && ks[i].T <= tmax)
       best = std::max(best, ks[i].T);
   return best;
 }
@@ -388,7 +390,7 @@ int alloc_work(int epochs, cudaStream_t st, int** out) {
 }
 
 int run_tb2d_stage(const ProblemDesc& p, const TbKernel* k, int epochs, int first_src,
-                   int first_dst, double* bufs[3], const CUtensorMap maps[3], bool coop_req,
+                   int first_dst, void* bufs[3], const CUtensorMap maps[3], bool coop_req,
                    int seg_rows_req, const DevInfo& di, cudaStream_t st, Counters* ctr) {
   const int n0 = (int)p.ext[0], n1 = (int)p.ext[1];
   const int T = k->T, R = p.rad;
@@ -502,7 +504,7 @@ int run_tb2d_stage(const ProblemDesc& p, const TbKernel* k, int epochs, int firs
 }
 
 int run_halo2d_stage(const ProblemDesc& p, const TbKernel* k, int epochs, int first_src,
-                     int first_dst, double* bufs[3], const CUtensorMap maps[3], bool coop_req,
+                     int first_dst, void* bufs[3], const CUtensorMap maps[3], bool coop_req,
                      int seg_rows_req, const DevInfo& di, cudaStream_t st, Counters* ctr) {
   const int n0 = (int)p.ext[0], n1 = (int)p.ext[1];
   const int T = k->T, R = p.rad;
@@ -599,7 +601,7 @@ int run_halo2d_stage(const ProblemDesc& p, const TbKernel* k, int epochs, int fi
 }
 
 int run_tb3d_stage(const ProblemDesc& p, const TbKernel* k, int epochs, int first_src,
-                   int first_dst, double* bufs[3], const CUtensorMap maps[3], bool coop_req,
+                   int first_dst, void* bufs[3], const CUtensorMap maps[3], bool coop_req,
                    int seg_rows_req, const DevInfo& di, cudaStream_t st, Counters* ctr) {
   const int n0 = (int)p.ext[0], n1 = (int)p.ext[1], n2 = (int)p.ext[2];
   const int T = k->T, R = p.rad;
@@ -700,7 +702,7 @@ int run_tb3d_stage(const ProblemDesc& p, const TbKernel* k, int epochs, int firs
   return EBISU_OK;
 }
 
-int run_device_impl(const ProblemDesc& p0, const double* d_in, double* d_out, double* d_scr,
+int run_device_impl(const ProblemDesc& p0, const void* d_in, void* d_out, void* d_scr,
                     long long steps, const ebisu_params* prm, cudaStream_t st, Counters* ctr) {
   ProblemDesc p = p0;
   const bool ranged = prm && prm->out_planes[1] > 0;
@@ -710,7 +712,7 @@ int run_device_impl(const ProblemDesc& p0, const double* d_in, double* d_out, do
   int rc = device_info(&di);
   if (rc) return rc;
   const long long total = p.ext[0] * p.ext[1] * p.ext[2];
-  const size_t bytes = (size_t)total * sizeof(double);
+  const size_t bytes = (size_t)total * (size_t)p.elem;
   if (steps == 0) {
     if (d_out != d_in) EB_CUDA(cudaMemcpyAsync(d_out, d_in, bytes, cudaMemcpyDeviceToDevice, st));
     return EBISU_OK;
@@ -725,7 +727,7 @@ int run_device_impl(const ProblemDesc& p0, const double* d_in, double* d_out, do
   const bool uni = uniform_coeffs(p) && !(prm && prm->per_tap_products);
   // TMA needs 16-byte row strides (even last extent) and 16-byte aligned bases.
   bool tb_ok = (D == 2 || D == 3) && p.shape_id != SHAPE_GENERIC &&
-               scheme != EBISU_SCHEME_NAIVE && (p.ext[D - 1] % 2 == 0) &&
+               scheme != EBISU_SCHEME_NAIVE && ((p.ext[D - 1] * p.elem) % 16 == 0) &&
                (reinterpret_cast<uintptr_t>(d_in) % 16 == 0) &&
                (reinterpret_cast<uintptr_t>(d_out) % 16 == 0) &&
                (!d_scr || reinterpret_cast<uintptr_t>(d_scr) % 16 == 0);
@@ -736,16 +738,16 @@ int run_device_impl(const ProblemDesc& p0, const double* d_in, double* d_out, do
     int fam = pick_family(scheme, p.shape_id, D);
     // no halo-exchange instantiation for this stencil/arithmetic: the
     // overlapped kernels compute the identical result
-    if (fam == 1 && best_depth_leq(p.shape_id, D, 64, exact, uni, 1) == 0) fam = 0;
-    const TbKernel* k = find_tb(p.shape_id, D, t, exact, uni, fam, want_c, want_v);
+    if (fam == 1 && best_depth_leq(p.shape_id, D, 64, exact, uni, 1, p.elem) == 0) fam = 0;
+    const TbKernel* k = find_tb(p.shape_id, D, t, exact, uni, fam, p.elem, want_c, want_v);
     if (!k && (want_c || want_v))
       return fail(EBISU_ERR_UNSUPPORTED, "no kernel with depth %d, %d cells per lane, variant %d",
                   t, want_c, want_v);
     if (!k) {
       // depth not instantiated: compose the sweep from the deepest kernel
       // below it (epochs compose bitwise, test_grid.py:94-117)
-      t = best_depth_leq(p.shape_id, D, t, exact, uni, fam);
-      k = t ? find_tb(p.shape_id, D, t, exact, uni, fam) : nullptr;
+      t = best_depth_leq(p.shape_id, D, t, exact, uni, fam, p.elem);
+      k = t ? find_tb(p.shape_id, D, t, exact, uni, fam, p.elem) : nullptr;
     }
     if (!k) {
       tb_ok = false;
@@ -755,13 +757,13 @@ int run_device_impl(const ProblemDesc& p0, const double* d_in, double* d_out, do
       const int kid = D == 3 ? KID_STREAM3D : (fam == 1 ? KID_HALO2D : KID_STREAM2D);
       if (full > 0) stages.push_back({kid, k, (int)full});
       while (rem > 0) {
-        const int t2 = best_depth_leq(p.shape_id, D, (int)rem, exact, uni, fam);
+        const int t2 = best_depth_leq(p.shape_id, D, (int)rem, exact, uni, fam, p.elem);
         if (t2 == 0) {
           stages.push_back({KID_NAIVE, nullptr, (int)rem});
           break;
         }
         const long long e2 = rem / t2;
-        stages.push_back({kid, find_tb(p.shape_id, D, t2, exact, uni, fam), (int)e2});
+        stages.push_back({kid, find_tb(p.shape_id, D, t2, exact, uni, fam, p.elem), (int)e2});
         rem -= e2 * t2;
       }
     }
@@ -779,13 +781,13 @@ int run_device_impl(const ProblemDesc& p0, const double* d_in, double* d_out, do
                 "output-plane range needs a single fused epoch (steps <= t with a kernel of "
                 "that depth), got %lld writes",
                 nwrites);
-  double* scr = d_scr;
+  void* scr = d_scr;
   bool own_scr = false;
   if (nwrites > 1 && !scr) {
-    EB_CUDA(cudaMallocAsync((void**)&scr, bytes, st));
+    EB_CUDA(cudaMallocAsync(&scr, bytes, st));
     own_scr = true;
   }
-  double* bufs[3] = {const_cast<double*>(d_in), d_out, scr};
+  void* bufs[3] = {const_cast<void*>(d_in), d_out, scr};
   CUtensorMap maps[3];
   // Shared-product kernels never store frame cells (their windows hold
   // products, not values); the frame is constant, so copy it once into both
@@ -839,7 +841,7 @@ int run_device_impl(const ProblemDesc& p0, const double* d_in, double* d_out, do
             memset(&maps[i], 0, sizeof(CUtensorMap));
             continue;
           }
-          result = encode_map(&maps[i], bufs[i], D, dims_ff, box);
+          result = encode_map(&maps[i], bufs[i], D, dims_ff, box, p.elem);
         }
         if (result) break;
       }
@@ -921,14 +923,16 @@ static void fill_trace(ebisu_trace* tr, const ProblemDesc& p, long long steps, c
   tr->warps_per_cta = c.nw;
 }
 
-int32_t ebisu_run_device(const ebisu_stencil* stencil, int32_t ndim, const int64_t* extents,
-                         const double* d_in, double* d_out, double* d_scratch, int64_t steps,
-                         const ebisu_params* params, void* stream, ebisu_trace* trace) {
+static int32_t run_device_entry(const ebisu_stencil* stencil, int32_t ndim,
+                                const int64_t* extents, const void* d_in, void* d_out,
+                                void* d_scratch, int64_t steps, const ebisu_params* params,
+                                void* stream, ebisu_trace* trace, int elem) {
   g_err.clear();
   if (steps < 0) return fail(EBISU_ERR_VALUE, "step count must be >= 0");
   ProblemDesc p;
   int rc = validate(stencil, ndim, extents, params, &p);
   if (rc) return rc;
+  p.elem = elem;
   if (!d_in || !d_out) return fail(EBISU_ERR_VALUE, "null device buffer");
   if (d_in == d_out && steps > 0)
     return fail(EBISU_ERR_VALUE, "d_in and d_out must be distinct (the input is read only)");
@@ -957,9 +961,9 @@ int32_t ebisu_run_device(const ebisu_stencil* stencil, int32_t ndim, const int64
   return rc;
 }
 
-int32_t ebisu_run_host(const ebisu_stencil* stencil, int32_t ndim, const int64_t* extents,
-                       const double* in, double* out, int64_t steps, const ebisu_params* params,
-                       ebisu_trace* trace) {
+static int32_t run_host_entry(const ebisu_stencil* stencil, int32_t ndim,
+                              const int64_t* extents, const void* in, void* out, int64_t steps,
+                              const ebisu_params* params, ebisu_trace* trace, int elem) {
   g_err.clear();
   if (steps < 0) return fail(EBISU_ERR_VALUE, "step count must be >= 0");
   ProblemDesc p;
@@ -967,18 +971,19 @@ int32_t ebisu_run_host(const ebisu_stencil* stencil, int32_t ndim, const int64_t
   if (rc) return rc;
   if (!in || !out) return fail(EBISU_ERR_VALUE, "null host buffer");
   if (ebisu_device_count() == 0) return fail(EBISU_ERR_NO_DEVICE, "no CUDA device visible");
-  const size_t bytes = (size_t)(p.ext[0] * p.ext[1] * p.ext[2]) * sizeof(double);
+  const size_t bytes = (size_t)(p.ext[0] * p.ext[1] * p.ext[2]) * (size_t)elem;
   cudaStream_t st = cudaStreamPerThread;
-  double *d_in = nullptr, *d_out = nullptr;
-  EB_CUDA(cudaMallocAsync((void**)&d_in, bytes, st));
-  cudaError_t e = cudaMallocAsync((void**)&d_out, bytes, st);
+  void *d_in = nullptr, *d_out = nullptr;
+  EB_CUDA(cudaMallocAsync(&d_in, bytes, st));
+  cudaError_t e = cudaMallocAsync(&d_out, bytes, st);
   if (e != cudaSuccess) {
     cudaFreeAsync(d_in, st);
     return cuda_fail(e, "cudaMallocAsync(out)");
   }
   e = cudaMemcpyAsync(d_in, in, bytes, cudaMemcpyHostToDevice, st);
   if (e == cudaSuccess) {
-    rc = ebisu_run_device(stencil, ndim, extents, d_in, d_out, nullptr, steps, params, st, trace);
+    rc = run_device_entry(stencil, ndim, extents, d_in, d_out, nullptr, steps, params, st, trace,
+                          elem);
     if (!rc) e = cudaMemcpyAsync(out, d_out, bytes, cudaMemcpyDeviceToHost, st);
   }
   if (e == cudaSuccess) e = cudaStreamSynchronize(st);
@@ -987,6 +992,32 @@ int32_t ebisu_run_host(const ebisu_stencil* stencil, int32_t ndim, const int64_t
   if (rc) return rc;
   if (e != cudaSuccess) return cuda_fail(e, "host<->device copy");
   return EBISU_OK;
+}
+
+int32_t ebisu_run_device(const ebisu_stencil* stencil, int32_t ndim, const int64_t* extents,
+                         const double* d_in, double* d_out, double* d_scratch, int64_t steps,
+                         const ebisu_params* params, void* stream, ebisu_trace* trace) {
+  return run_device_entry(stencil, ndim, extents, d_in, d_out, d_scratch, steps, params, stream,
+                          trace, 8);
+}
+
+int32_t ebisu_run_device_f32(const ebisu_stencil* stencil, int32_t ndim, const int64_t* extents,
+                             const float* d_in, float* d_out, float* d_scratch, int64_t steps,
+                             const ebisu_params* params, void* stream, ebisu_trace* trace) {
+  return run_device_entry(stencil, ndim, extents, d_in, d_out, d_scratch, steps, params, stream,
+                          trace, 4);
+}
+
+int32_t ebisu_run_host(const ebisu_stencil* stencil, int32_t ndim, const int64_t* extents,
+                       const double* in, double* out, int64_t steps, const ebisu_params* params,
+                       ebisu_trace* trace) {
+  return run_host_entry(stencil, ndim, extents, in, out, steps, params, trace, 8);
+}
+
+int32_t ebisu_run_host_f32(const ebisu_stencil* stencil, int32_t ndim, const int64_t* extents,
+                           const float* in, float* out, int64_t steps, const ebisu_params* params,
+                           ebisu_trace* trace) {
+  return run_host_entry(stencil, ndim, extents, in, out, steps, params, trace, 4);
 }
 
 int32_t ebisu_random_grid_device(uint64_t seed, int64_t start, int64_t n, double* d_out,

@@ -108,28 +108,82 @@ __device__ __forceinline__ void prefetch_tmap(const CUtensorMap* map) {
   asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(map)) : "memory");
 }
 
+// ---- element type (fp64: the reference's arithmetic; fp32: the north-star
+// 1e-5 mode) ------------------------------------------------------------------
+template <class E>
+struct Vec2;
+template <>
+struct Vec2<double> {
+  using type = double2;
+};
+template <>
+struct Vec2<float> {
+  using type = float2;
+};
+template <class E>
+using vec2_t = typename Vec2<E>::type;
+template <class E>
+__device__ __forceinline__ vec2_t<E> make_v2(E a, E b) {
+  vec2_t<E> r;
+  r.x = a;
+  r.y = b;
+  return r;
+}
+
+template <class E>
+__device__ __forceinline__ E mul_rn(E a, E b);
+template <>
+__device__ __forceinline__ double mul_rn<double>(double a, double b) {
+  return __dmul_rn(a, b);
+}
+template <>
+__device__ __forceinline__ float mul_rn<float>(float a, float b) {
+  return __fmul_rn(a, b);
+}
+template <class E>
+__device__ __forceinline__ E add_rn(E a, E b);
+template <>
+__device__ __forceinline__ double add_rn<double>(double a, double b) {
+  return __dadd_rn(a, b);
+}
+template <>
+__device__ __forceinline__ float add_rn<float>(float a, float b) {
+  return __fadd_rn(a, b);
+}
+template <class E>
+__device__ __forceinline__ E fma_rn(E a, E b, E c);
+template <>
+__device__ __forceinline__ double fma_rn<double>(double a, double b, double c) {
+  return __fma_rn(a, b, c);
+}
+template <>
+__device__ __forceinline__ float fma_rn<float>(float a, float b, float c) {
+  return __fmaf_rn(a, b, c);
+}
+
 // ---- tap accumulation -----------------------------------------------------
 // EXACT: acc = c0*x0; acc = acc + ck*xk -- each op separately rounded, i.e.
 // exactly numpy's `term = c * cells[sl]; acc = acc + term` (grid.py:87-92).
 // Not EXACT: contracted FMA chain (tolerance mode, 1e-12 relative).
-template <bool EXACT>
-__device__ __forceinline__ double tap_first(double c, double x) {
-  return __dmul_rn(c, x);
+template <bool EXACT, class E>
+__device__ __forceinline__ E tap_first(E c, E x) {
+  return mul_rn<E>(c, x);
 }
-template <bool EXACT>
-__device__ __forceinline__ double tap_next(double acc, double c, double x) {
+template <bool EXACT, class E>
+__device__ __forceinline__ E tap_next(E acc, E c, E x) {
   if constexpr (EXACT) {
-    return __dadd_rn(acc, __dmul_rn(c, x));
+    return add_rn<E>(acc, mul_rn<E>(c, x));
   } else {
-    return __fma_rn(c, x, acc);
+    return fma_rn<E>(c, x, acc);
   }
 }
 
 // Coefficients travel in the kernel parameter space (constant bank), so the
-// DMUL operands come straight from c[0x0][...] without occupying registers.
-template <int NT>
+// multiply operands come straight from c[0x0][...] without occupying
+// registers.  fp32 kernels get the coefficients rounded to float once.
+template <int NT, class E = double>
 struct Coefs {
-  double c[NT];
+  E c[NT];
 };
 
 struct alignas(64) TmapSet {

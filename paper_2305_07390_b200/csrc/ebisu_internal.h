@@ -27,11 +27,12 @@ struct ProblemDesc {
   const double* coeffs;  // [ntaps]
   int shape_id;          // ShapeId or SHAPE_GENERIC
   int z_lo = 0, z_hi = 0;  // output planes [z_lo, z_hi) along axis 0 (set by the driver)
+  int elem = 8;            // element bytes: 8 (fp64) or 4 (fp32)
 };
 
-cudaError_t launch_naive_step(const ProblemDesc& p, const double* in, double* out, bool exact,
+cudaError_t launch_naive_step(const ProblemDesc& p, const void* in, void* out, bool exact,
                               cudaStream_t st, int num_sms);  // writes planes [z_lo, z_hi)
-cudaError_t launch_frame_copy(const ProblemDesc& p, const double* in, double* out,
+cudaError_t launch_frame_copy(const ProblemDesc& p, const void* in, void* out,
                               cudaStream_t st, int num_sms);
 cudaError_t launch_splitmix(unsigned long long seed, long long start, long long n, double* out,
                             cudaStream_t st, int num_sms);
@@ -51,7 +52,7 @@ struct TbLaunch {
   const int* seg_start;        // 3-D: nseg+1 segment bounds along axis 0 (guided)
   int epochs;
   int first_src, first_dst;
-  double* buf[3];
+  void* buf[3];  // element type of the stage's kernel
   const CUtensorMap* maps;  // host copies [3]
   const double* coeffs;
   int grid;
@@ -79,6 +80,7 @@ struct TbKernel {
   const void* func;      // kernel symbol (occupancy queries / attributes)
   cudaError_t (*launch)(const TbLaunch&);
   int family;            // 0: overlapped (sm-tiling), 1: halo exchange (device-tiling)
+  int elem;              // element bytes: 8 (fp64) or 4 (fp32)
 };
 
 // All instantiated temporal-blocking kernels (ebisu_registry.cu).

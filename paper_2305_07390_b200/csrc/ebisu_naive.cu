@@ -21,9 +21,9 @@ struct NaiveTaps {
   double coef[EBISU_MAX_TAPS];
 };
 
-template <bool EXACT>
-__global__ void __launch_bounds__(256) k_naive_step(const double* __restrict__ in,
-                                                    double* __restrict__ out,
+template <bool EXACT, class E>
+__global__ void __launch_bounds__(256) k_naive_step(const E* __restrict__ in,
+                                                    E* __restrict__ out,
                                                     const __grid_constant__ NaiveTaps tp) {
   const long long plane = tp.n1 * tp.n2;
   const long long base = tp.z_lo * plane;
@@ -39,19 +39,19 @@ __global__ void __launch_bounds__(256) k_naive_step(const double* __restrict__ i
     bool frame = (i0 < R) || (i0 >= tp.n0 - R);
     if (tp.dims >= 2) frame |= (i1 < R) || (i1 >= tp.n1 - R);
     if (tp.dims >= 3) frame |= (i2 < R) || (i2 >= tp.n2 - R);
-    double v;
+    E v;
     if (frame) {
       v = in[idx];
     } else {
-      v = tap_first<EXACT>(tp.coef[0], __ldg(in + idx + tp.lin[0]));
+      v = tap_first<EXACT, E>((E)tp.coef[0], __ldg(in + idx + tp.lin[0]));
       for (int t = 1; t < tp.ntaps; ++t)
-        v = tap_next<EXACT>(v, tp.coef[t], __ldg(in + idx + tp.lin[t]));
+        v = tap_next<EXACT, E>(v, (E)tp.coef[t], __ldg(in + idx + tp.lin[t]));
     }
     out[idx] = v;
   }
 }
 
-cudaError_t launch_naive_step(const ProblemDesc& p, const double* in, double* out,
+cudaError_t launch_naive_step(const ProblemDesc& p, const void* in, void* out,
                               bool exact, cudaStream_t st, int num_sms) {
   NaiveTaps tp{};
   tp.ntaps = p.ntaps;
@@ -75,10 +75,21 @@ cudaError_t launch_naive_step(const ProblemDesc& p, const double* in, double* ou
   const long long cap = (long long)num_sms * 8;
   if (blocks > cap) blocks = cap;
   if (blocks < 1) blocks = 1;
-  if (exact)
-    k_naive_step<true><<<(unsigned)blocks, 256, 0, st>>>(in, out, tp);
-  else
-    k_naive_step<false><<<(unsigned)blocks, 256, 0, st>>>(in, out, tp);
+  if (p.elem == 4) {
+    const float* fi = static_cast<const float*>(in);
+    float* fo = static_cast<float*>(out);
+    if (exact)
+      k_naive_step<true, float><<<(unsigned)blocks, 256, 0, st>>>(fi, fo, tp);
+    else
+      k_naive_step<false, float><<<(unsigned)blocks, 256, 0, st>>>(fi, fo, tp);
+  } else {
+    const double* di = static_cast<const double*>(in);
+    double* dout = static_cast<double*>(out);
+    if (exact)
+      k_naive_step<true, double><<<(unsigned)blocks, 256, 0, st>>>(di, dout, tp);
+    else
+      k_naive_step<false, double><<<(unsigned)blocks, 256, 0, st>>>(di, dout, tp);
+  }
   return cudaGetLastError();
 }
 
@@ -86,8 +97,9 @@ cudaError_t launch_naive_step(const ProblemDesc& p, const double* in, double* ou
 // Copies the Dirichlet frame (cells within R of any face, common.py:96-112)
 // from `in` to `out`.  One warp per row of the fastest axis: frame rows are
 // copied whole, other rows only their first and last R cells.
-__global__ void __launch_bounds__(256) k_frame_copy(const double* __restrict__ in,
-                                                    double* __restrict__ out, long long P,
+template <class E>
+__global__ void __launch_bounds__(256) k_frame_copy(const E* __restrict__ in,
+                                                    E* __restrict__ out, long long P,
                                                     long long Y, long long X, int R0, int R1,
                                                     int R2, long long row_lo, long long row_hi) {
   const int lane = threadIdx.x & 31;
@@ -95,8 +107,8 @@ __global__ void __launch_bounds__(256) k_frame_copy(const double* __restrict__ i
   for (long long row = row_lo + (long long)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
        row < row_hi; row += warps) {
     const long long pp = row / Y, y = row % Y;
-    const double* src = in + row * X;
-    double* dst = out + row * X;
+    const E* src = in + row * X;
+    E* dst = out + row * X;
     if (pp < R0 || pp >= P - R0 || y < R1 || y >= Y - R1) {
       for (long long j = lane; j < X; j += 32) dst[j] = src[j];
     } else {
@@ -108,7 +120,7 @@ __global__ void __launch_bounds__(256) k_frame_copy(const double* __restrict__ i
   }
 }
 
-cudaError_t launch_frame_copy(const ProblemDesc& p, const double* in, double* out,
+cudaError_t launch_frame_copy(const ProblemDesc& p, const void* in, void* out,
                               cudaStream_t st, int num_sms) {
   long long P = 1, Y = 1, X = p.ext[0];
   int R0 = 0, R1 = 0;
@@ -132,8 +144,14 @@ cudaError_t launch_frame_copy(const ProblemDesc& p, const double* in, double* ou
   const long long cap = (long long)num_sms * 8;
   if (blocks > cap) blocks = cap;
   if (blocks < 1) blocks = 1;
-  k_frame_copy<<<(unsigned)blocks, 256, 0, st>>>(in, out, P, Y, X, R0, R1, p.rad, row_lo,
-                                                 row_hi);
+  if (p.elem == 4)
+    k_frame_copy<float><<<(unsigned)blocks, 256, 0, st>>>(
+        static_cast<const float*>(in), static_cast<float*>(out), P, Y, X, R0, R1, p.rad, row_lo,
+        row_hi);
+  else
+    k_frame_copy<double><<<(unsigned)blocks, 256, 0, st>>>(
+        static_cast<const double*>(in), static_cast<double*>(out), P, Y, X, R0, R1, p.rad, row_lo,
+        row_hi);
   return cudaGetLastError();
 }
 

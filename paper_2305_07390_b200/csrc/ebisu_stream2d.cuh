@@ -60,21 +60,22 @@ struct Stream2DArgs {
   int first_src;     // BufId of epoch 0's source
   int first_dst;     // BufId of epoch 0's destination
   int aligned;       // 1: edge-aligned strips (n1 >= 2*LC); 0: generic strips
-  double* buf[3];    // device pointers by BufId
+  void* buf[3];      // device pointers by BufId (element type E of the kernel)
   long long* unit_clock;  // optional profiling: [units][2] start/end globaltimer (ns)
   int* work;         // per-epoch unit counters (dynamic scheduling), zeroed by the host
 };
 
-template <class SH, int T, int C, int NW, int S>
+template <class SH, int T, int C, int NW, int S, class E = double>
 struct Stream2DCfg {
   static constexpr int R = SH::R;
   static constexpr int W = 2 * R + 1;       // window rows per level
   static constexpr int LC = 32 * C;         // loaded columns per warp
   // Column halo rounded up to even: a TMA box must start on a 16-byte
-  // boundary in the innermost dimension (2 doubles).
-  static constexpr int HX = (T * R + 1) & ~1;
+  // boundary in the innermost dimension (2 doubles / 4 floats).
+  static constexpr int AL = 16 / (int)sizeof(E);
+  static constexpr int HX = (T * R + AL - 1) / AL * AL;
   static constexpr int VW = LC - 2 * HX;    // valid columns per warp (even)
-  static constexpr int ROW_BYTES = LC * 8;
+  static constexpr int ROW_BYTES = LC * (int)sizeof(E);
   static constexpr int RING_BYTES = S * ROW_BYTES;
   static constexpr int SMEM_BYTES = NW * RING_BYTES + NW * S * 8;
   static_assert(VW > 0, "tile leaves no valid core");
@@ -143,15 +144,15 @@ __host__ __device__ constexpr int pmod(int a) {
 
 // One work unit (warp strip x row segment) of one epoch.  FC selects the
 // frame-column handling (see StripGeom); frame rows are handled per block.
-template <class SH, int T, int C, int S, bool EXACT, bool UNI, int FC>
-__device__ __forceinline__ void stream2d_unit(const CUtensorMap* tm, double* __restrict__ out,
-                                              double* ring, uint64_t* bars, uint32_t ring_cnt,
+template <class SH, int T, int C, int S, bool EXACT, bool UNI, int FC, class E>
+__device__ __forceinline__ void stream2d_unit(const CUtensorMap* tm, E* __restrict__ out,
+                                              E* ring, uint64_t* bars, uint32_t ring_cnt,
                                               int lane, int n0, int n1, const StripGeom& g,
-                                              int r0, int r1, const Coefs<SH::NT>& cf) {
+                                              int r0, int r1, const Coefs<SH::NT, E>& cf) {
   constexpr int R = SH::R;
   constexpr int W = 2 * R + 1;
   constexpr int LC = 32 * C;
-  constexpr int ROW_BYTES = LC * 8;
+  constexpr int ROW_BYTES = LC * (int)sizeof(E);
   constexpr int TR = T * R;
   static_assert(FC == 0 || FC == 3 || R <= C, "frame columns must fit in one lane");
 
@@ -189,7 +190,7 @@ __device__ __forceinline__ void stream2d_unit(const CUtensorMap* tm, double* __r
     return FC == 3 || (FC == 1 && c < R) || (FC == 2 && c >= C - R);
   };
 
-  double win[T][W][C];
+  E win[T][W][C];
 #pragma unroll
   for (int s = 0; s < T; ++s)
 #pragma unroll
@@ -208,7 +209,7 @@ __device__ __forceinline__ void stream2d_unit(const CUtensorMap* tm, double* __r
       // (the select keeps the window write unconditional, so the dead oldest
       // row never stays live across the advance)
       {
-        double v[C];
+        E v[C];
         if (k < kb) {
           const uint32_t pos = ring_cnt + (uint32_t)(k - ka);
           const uint32_t slot = pos & (S - 1);
@@ -221,11 +222,11 @@ __device__ __forceinline__ void stream2d_unit(const CUtensorMap* tm, double* __r
             mbar_arrive_expect_tx(&bars[ps], ROW_BYTES);
             tma_load_2d(ring + ps * LC, tm, X0, k - 1 + S, &bars[ps]);
           }
-          const double* rowp = ring + slot * LC + lane * C;
+          const E* rowp = ring + slot * LC + lane * C;
           if constexpr (C % 2 == 0) {
 #pragma unroll
             for (int c = 0; c < C; c += 2) {
-              const double2 t2 = *reinterpret_cast<const double2*>(rowp + c);
+              const vec2_t<E> t2 = *reinterpret_cast<const vec2_t<E>*>(rowp + c);
               v[c] = t2.x;
               v[c + 1] = t2.y;
             }
@@ -239,7 +240,7 @@ __device__ __forceinline__ void stream2d_unit(const CUtensorMap* tm, double* __r
         }
         // UNI: the window holds products y = c*x (one DMUL per cell per level)
 #pragma unroll
-        for (int c = 0; c < C; ++c) win[0][uu][c] = UNI ? __dmul_rn(cf.c[0], v[c]) : v[c];
+        for (int c = 0; c < C; ++c) win[0][uu][c] = UNI ? mul_rn<E>(cf.c[0], v[c]) : v[c];
       }
       // ---- levels 1..T ----------------------------------------------------
       // Every level runs every advance.  During pipeline warm-up a level's
@@ -251,7 +252,7 @@ __device__ __forceinline__ void stream2d_unit(const CUtensorMap* tm, double* __r
         constexpr int s = decltype(sI)::value + 1;  // level being produced
         const int q = k - s * R;                    // its target row
         // horizontal halos (only rows whose taps leave the lane's columns)
-        double hl[W][R], hr[W][R];
+        E hl[W][R], hr[W][R];
         static_for<W>([&](auto wI) {
           constexpr int dy = decltype(wI)::value - R;
           if constexpr (row_has_halo<SH>(dy)) {
@@ -270,7 +271,7 @@ __device__ __forceinline__ void stream2d_unit(const CUtensorMap* tm, double* __r
           }
         });
         // tap-major order: the C per-column chains are independent
-        double acc[C];
+        E acc[C];
         static_for<SH::NT>([&](auto iI) {
           constexpr int i = decltype(iI)::value;
           constexpr Off o = SH::tap(i);
@@ -278,7 +279,7 @@ __device__ __forceinline__ void stream2d_unit(const CUtensorMap* tm, double* __r
           for (int c = 0; c < C; ++c) {
             const int sl = pmod<W>(uu - s * R + o.d0);
             const int cc = c + o.d1;
-            double x;
+            E x;
             if (cc < 0)
               x = hl[o.d0 + R][cc + R];
             else if (cc >= C)
@@ -286,7 +287,7 @@ __device__ __forceinline__ void stream2d_unit(const CUtensorMap* tm, double* __r
             else
               x = win[s - 1][sl][cc];
             if constexpr (UNI)
-              acc[c] = (i == 0) ? x : __dadd_rn(acc[c], x);
+              acc[c] = (i == 0) ? x : add_rn<E>(acc[c], x);
             else if constexpr (i == 0)
               acc[c] = tap_first<EXACT>(cf.c[0], x);
             else
@@ -297,13 +298,13 @@ __device__ __forceinline__ void stream2d_unit(const CUtensorMap* tm, double* __r
         // mode the carried centre is the product c*x, which is the frame's
         // product at every level, and level T never stores frame cells (the
         // host pre-copies the frame into both ping-pong buffers)
-        double nv[C];
+        E nv[C];
         bool frow = false;
         if constexpr (FROWS) frow = (q < R) || (q >= n0 - R);
 #pragma unroll
         for (int c = 0; c < C; ++c) {
-          const double centre = win[s - 1][pmod<W>(uu - s * R)][c];
-          const double val = (UNI && s < T) ? __dmul_rn(cf.c[0], acc[c]) : acc[c];
+          const E centre = win[s - 1][pmod<W>(uu - s * R)][c];
+          const E val = (UNI && s < T) ? mul_rn<E>(cf.c[0], acc[c]) : acc[c];
           if (FROWS && col_may_frame(c))
             nv[c] = (frow || fcol[c]) ? centre : val;
           else if (FROWS)
@@ -318,7 +319,7 @@ __device__ __forceinline__ void stream2d_unit(const CUtensorMap* tm, double* __r
           for (int c = 0; c < C; ++c) win[s][pmod<W>(uu - s * R)][c] = nv[c];
         } else {
           if (q >= r0 && q < r1) {
-            double* orow = out + (size_t)q * (size_t)n1 + (X0 + lane * C);
+            E* orow = out + (size_t)q * (size_t)n1 + (X0 + lane * C);
 #pragma unroll
             for (int c = 0; c < C; ++c) {
               bool st = stcol[c];
@@ -351,18 +352,18 @@ __device__ __forceinline__ int next_unit(int* counter, int lane) {
   return __shfl_sync(kFullMask, u, 0);
 }
 
-template <class SH, int T, int C, int NW, int S, bool EXACT, bool UNI, int MINB>
+template <class SH, int T, int C, int NW, int S, bool EXACT, bool UNI, int MINB, class E = double>
 __global__ void __launch_bounds__(NW * 32, MINB)
     k_stream2d(const __grid_constant__ TmapSet maps, const Stream2DArgs a,
-               const __grid_constant__ Coefs<SH::NT> cf) {
-  using Cfg = Stream2DCfg<SH, T, C, NW, S>;
+               const __grid_constant__ Coefs<SH::NT, E> cf) {
+  using Cfg = Stream2DCfg<SH, T, C, NW, S, E>;
   constexpr int R = Cfg::R;
   constexpr int TR = T * R;
 
   extern __shared__ __align__(1024) unsigned char smem[];
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
-  double* ring = reinterpret_cast<double*>(smem + warp * Cfg::RING_BYTES);
+  E* ring = reinterpret_cast<E*>(smem + warp * Cfg::RING_BYTES);
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem + NW * Cfg::RING_BYTES) + warp * S;
 
   if (lane == 0) {
@@ -382,7 +383,7 @@ __global__ void __launch_bounds__(NW * 32, MINB)
   int src = a.first_src, dst = a.first_dst;
   for (int e = 0; e < a.epochs; ++e) {
     const CUtensorMap* tm = &maps.m[src];
-    double* __restrict__ out = (dst == BUF_OUT) ? a.buf[BUF_OUT] : a.buf[BUF_SCR];
+    E* __restrict__ out = static_cast<E*>((dst == BUF_OUT) ? a.buf[BUF_OUT] : a.buf[BUF_SCR]);
 
     // Dynamic unit distribution: a warp grabs the next unit when it finishes
     // one, so warps the scheduler favours take more units and the epoch tail
@@ -400,23 +401,23 @@ __global__ void __launch_bounds__(NW * 32, MINB)
       if (a.unit_clock && e == 0 && lane == 0)
         asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_start));
       if constexpr (R > C) {
-        stream2d_unit<SH, T, C, S, EXACT, UNI, 3>(tm, out, ring, bars, ring_cnt, lane, n0, n1, g, r0,
+        stream2d_unit<SH, T, C, S, EXACT, UNI, 3, E>(tm, out, ring, bars, ring_cnt, lane, n0, n1, g, r0,
                                              r1, cf);
       } else switch (g.fc) {
         case 0:
-          stream2d_unit<SH, T, C, S, EXACT, UNI, 0>(tm, out, ring, bars, ring_cnt, lane, n0, n1, g,
+          stream2d_unit<SH, T, C, S, EXACT, UNI, 0, E>(tm, out, ring, bars, ring_cnt, lane, n0, n1, g,
                                                r0, r1, cf);
           break;
         case 1:
-          stream2d_unit<SH, T, C, S, EXACT, UNI, 1>(tm, out, ring, bars, ring_cnt, lane, n0, n1, g,
+          stream2d_unit<SH, T, C, S, EXACT, UNI, 1, E>(tm, out, ring, bars, ring_cnt, lane, n0, n1, g,
                                                r0, r1, cf);
           break;
         case 2:
-          stream2d_unit<SH, T, C, S, EXACT, UNI, 2>(tm, out, ring, bars, ring_cnt, lane, n0, n1, g,
+          stream2d_unit<SH, T, C, S, EXACT, UNI, 2, E>(tm, out, ring, bars, ring_cnt, lane, n0, n1, g,
                                                r0, r1, cf);
           break;
         default:
-          stream2d_unit<SH, T, C, S, EXACT, UNI, 3>(tm, out, ring, bars, ring_cnt, lane, n0, n1, g,
+          stream2d_unit<SH, T, C, S, EXACT, UNI, 3, E>(tm, out, ring, bars, ring_cnt, lane, n0, n1, g,
                                                r0, r1, cf);
           break;
       }

@@ -45,7 +45,7 @@ struct Stream3DArgs {
   int seg_start[EBISU_MAX_SEGS + 1];
   int epochs;
   int first_src, first_dst;
-  double* buf[3];
+  void* buf[3];  // element type E of the kernel
   int* work;  // per-epoch unit counters (dynamic scheduling), zeroed by the host
 };
 
@@ -80,7 +80,7 @@ __host__ __device__ constexpr bool row_needs_x_halo(int dz, int ey, int CY) {
   return false;
 }
 
-template <class SH, int T, int CY, int CX, int NWY, int S, int FL = 0>
+template <class SH, int T, int CY, int CX, int NWY, int S, int FL = 0, class E = double>
 struct Stream3DCfg {
   static constexpr int R = SH::R;
   static constexpr int Z = (offcentre_inplane<SH>() || (FL & 1)) ? R + 1 : R;  // level skew
@@ -89,16 +89,17 @@ struct Stream3DCfg {
   static constexpr int LY = NWY * CY;
   static constexpr int LX = 32 * CX;
   static constexpr int HY = T * R;
-  static constexpr int HX = (T * R + 1) & ~1;  // TMA: 16-byte aligned box start
+  static constexpr int AL = 16 / (int)sizeof(E);
+  static constexpr int HX = (T * R + AL - 1) / AL * AL;  // TMA: 16-byte aligned box start
   static constexpr int VY = LY - 2 * HY;
   static constexpr int VX = LX - 2 * HX;
   // Halo buffer: per warp, its top R and bottom R rows of a level's plane
   // ("push halo"); neighbours along axis 2 come from warp shuffles.
   static constexpr int HROWW = 2 * R;                 // rows per warp
   static constexpr int HPLANE = NWY * HROWW * LX;     // doubles per halo buffer
-  static constexpr int RING_PLANE = LY * LX;          // doubles per ring slot
-  static constexpr int RING_BYTES = S * RING_PLANE * 8;
-  static constexpr int HALO_BYTES = T * NB * HPLANE * 8;
+  static constexpr int RING_PLANE = LY * LX;          // elements per ring slot
+  static constexpr int RING_BYTES = S * RING_PLANE * (int)sizeof(E);
+  static constexpr int HALO_BYTES = T * NB * HPLANE * (int)sizeof(E);
   static constexpr int SMEM_BYTES = RING_BYTES + HALO_BYTES + S * 8;
   static_assert(CY >= R, "a warp's rows must cover the radius");
   static_assert(VY > 0 && VX > 0, "tile leaves no valid core");
@@ -122,17 +123,18 @@ __host__ __device__ inline int stream3d_advances(int ka, int r1, int TZ) {
 // are handled per block of WN advances (FPL), so z-edge segments cost the same
 // as interior ones outside their first and last blocks.  Returns the planes
 // consumed from the ring.
-template <class SH, int T, int CY, int CX, int NWY, int S, int FL, bool EXACT, bool UNI, bool EDGE>
-__device__ __forceinline__ int stream3d_unit(const CUtensorMap* tm, double* __restrict__ out,
-                                             double* ring, double* halo, uint64_t* bars,
+template <class SH, int T, int CY, int CX, int NWY, int S, int FL, bool EXACT, bool UNI, bool EDGE,
+          class E>
+__device__ __forceinline__ int stream3d_unit(const CUtensorMap* tm, E* __restrict__ out,
+                                             E* ring, E* halo, uint64_t* bars,
                                              uint32_t ring_cnt, int warp, int lane, int n0,
                                              int n1, int n2, int X0, int Y0, int xlo, int xhi,
                                              int ylo, int yhi, int r0, int r1,
-                                             const Coefs<SH::NT>& cf) {
-  using Cfg = Stream3DCfg<SH, T, CY, CX, NWY, S, FL>;
+                                             const Coefs<SH::NT, E>& cf) {
+  using Cfg = Stream3DCfg<SH, T, CY, CX, NWY, S, FL, E>;
   constexpr int R = Cfg::R, Z = Cfg::Z, WN = Cfg::WN, NB = Cfg::NB;
   constexpr int LY = Cfg::LY, LX = Cfg::LX;
-  constexpr int PLANE_BYTES = LY * LX * 8;
+  constexpr int PLANE_BYTES = LY * LX * (int)sizeof(E);
   constexpr int TZ = T * Z;  // pipeline depth along z
   static_assert(CY * CX <= 32, "cell masks are 32-bit");
 
@@ -165,7 +167,7 @@ __device__ __forceinline__ int stream3d_unit(const CUtensorMap* tm, double* __re
       stmask |= (uint32_t)st << (cy * CX + cx);
     }
 
-  double win[T][WN][CY][CX];
+  E win[T][WN][CY][CX];
 #pragma unroll
   for (int s = 0; s < T; ++s)
 #pragma unroll
@@ -176,19 +178,19 @@ __device__ __forceinline__ int stream3d_unit(const CUtensorMap* tm, double* __re
         for (int cx = 0; cx < CX; ++cx) win[s][w][cy][cx] = 0.0;
 
   // Halo buffer (level, b): warp-major [NWY][2R][LX]; this thread's columns.
-  auto hrow = [&](int level, int b, int w, int r) -> double* {
+  auto hrow = [&](int level, int b, int w, int r) -> E* {
     return halo + (size_t)(level * NB + b) * Cfg::HPLANE + (size_t)(w * 2 * R + r) * LX + tx0;
   };
   // push: top R rows and bottom R rows of this thread's block
-  auto push = [&](int level, int b, const double (&v)[CY][CX]) {
+  auto push = [&](int level, int b, const E (&v)[CY][CX]) {
     static_for<2 * R>([&](auto rI) {
       constexpr int r = decltype(rI)::value;
       constexpr int cy = r < R ? r : CY - 2 * R + r;
-      double* d = hrow(level, b, warp, r);
+      E* d = hrow(level, b, warp, r);
       if constexpr (CX % 2 == 0) {
 #pragma unroll
         for (int cx = 0; cx < CX; cx += 2)
-          *reinterpret_cast<double2*>(d + cx) = make_double2(v[cy][cx], v[cy][cx + 1]);
+          *reinterpret_cast<vec2_t<E>*>(d + cx) = make_v2<E>(v[cy][cx], v[cy][cx + 1]);
       } else {
 #pragma unroll
         for (int cx = 0; cx < CX; ++cx) d[cx] = v[cy][cx];
@@ -203,7 +205,7 @@ __device__ __forceinline__ int stream3d_unit(const CUtensorMap* tm, double* __re
 
   // output pointer of this thread's first cell in plane q = k - T*Z
   const long long plane = (long long)n1 * (long long)n2;
-  double* obase = out + ((long long)(Y0 + ty0) * n2 + (X0 + tx0));
+  E* obase = out + ((long long)(Y0 + ty0) * n2 + (X0 + tx0));
 
   auto block = [&](int kbase, auto fpl_tag) {
     constexpr bool FPL = decltype(fpl_tag)::value;  // a target plane may be a frame plane
@@ -213,17 +215,17 @@ __device__ __forceinline__ int stream3d_unit(const CUtensorMap* tm, double* __re
       const int bk = k % NB;  // halo buffer written this advance
       // ---- level 0 ----------------------------------------------------------
       {
-        double v[CY][CX];
+        E v[CY][CX];
         const uint32_t pos = ring_cnt + (uint32_t)(k - ka);
         const uint32_t slot = pos & (S - 1);
         mbar_wait(&bars[slot], (pos / S) & 1);
-        const double* p = ring + slot * Cfg::RING_PLANE + ty0 * LX + tx0;
+        const E* p = ring + slot * Cfg::RING_PLANE + ty0 * LX + tx0;
 #pragma unroll
         for (int cy = 0; cy < CY; ++cy) {
           if constexpr (CX % 2 == 0) {
 #pragma unroll
             for (int cx = 0; cx < CX; cx += 2) {
-              const double2 t2 = *reinterpret_cast<const double2*>(p + cy * LX + cx);
+              const vec2_t<E> t2 = *reinterpret_cast<const vec2_t<E>*>(p + cy * LX + cx);
               v[cy][cx] = t2.x;
               v[cy][cx + 1] = t2.y;
             }
@@ -237,7 +239,7 @@ __device__ __forceinline__ int stream3d_unit(const CUtensorMap* tm, double* __re
 #pragma unroll
           for (int cy = 0; cy < CY; ++cy)
 #pragma unroll
-            for (int cx = 0; cx < CX; ++cx) v[cy][cx] = __dmul_rn(cf.c[0], v[cy][cx]);
+            for (int cx = 0; cx < CX; ++cx) v[cy][cx] = mul_rn<E>(cf.c[0], v[cy][cx]);
         }
 #pragma unroll
         for (int cy = 0; cy < CY; ++cy)
@@ -251,11 +253,11 @@ __device__ __forceinline__ int stream3d_unit(const CUtensorMap* tm, double* __re
         const int q = k - s * Z;  // target plane of level s
         bool fpl = false;         // frame plane: every cell carries level s-1
         if constexpr (FPL) fpl = (q < R) || (q >= n0 - R);
-        double nv[CY][CX];
+        E nv[CY][CX];
         {
           // extended neighbourhood of the planes that need in-plane values:
           // ext[dz][cy+R][cx+R], cy in [-R, CY+R), cx in [-R, CX+R)
-          double ext[2 * R + 1][CY + 2 * R][CX + 2 * R];
+          E ext[2 * R + 1][CY + 2 * R][CX + 2 * R];
           static_for<2 * R + 1>([&](auto zI) {
             constexpr int dz = decltype(zI)::value - R;
             if constexpr (plane_needs_inplane<SH>(dz)) {
@@ -268,13 +270,13 @@ __device__ __forceinline__ int stream3d_unit(const CUtensorMap* tm, double* __re
               // rows above / below from the halo buffer
 #pragma unroll
               for (int r = 0; r < R; ++r) {
-                const double* up = hrow(s - 1, b, wa, warp > 0 ? R + r : r);
-                const double* dn = hrow(s - 1, b, wbl, warp < NWY - 1 ? r : R + r);
+                const E* up = hrow(s - 1, b, wa, warp > 0 ? R + r : r);
+                const E* dn = hrow(s - 1, b, wbl, warp < NWY - 1 ? r : R + r);
                 if constexpr (CX % 2 == 0) {
 #pragma unroll
                   for (int cx = 0; cx < CX; cx += 2) {
-                    const double2 a2 = *reinterpret_cast<const double2*>(up + cx);
-                    const double2 b2 = *reinterpret_cast<const double2*>(dn + cx);
+                    const vec2_t<E> a2 = *reinterpret_cast<const vec2_t<E>*>(up + cx);
+                    const vec2_t<E> b2 = *reinterpret_cast<const vec2_t<E>*>(dn + cx);
                     ext[zI][r][cx + R] = a2.x;
                     ext[zI][r][cx + 1 + R] = a2.y;
                     ext[zI][CY + R + r][cx + R] = b2.x;
@@ -307,7 +309,7 @@ __device__ __forceinline__ int stream3d_unit(const CUtensorMap* tm, double* __re
             }
           });
           // tap-major: CY*CX independent chains interleave in the instruction stream
-          double acc[CY][CX];
+          E acc[CY][CX];
           static_for<SH::NT>([&](auto iI) {
             constexpr int i = decltype(iI)::value;
             constexpr Off o = SH::tap(i);
@@ -315,13 +317,13 @@ __device__ __forceinline__ int stream3d_unit(const CUtensorMap* tm, double* __re
             for (int cy = 0; cy < CY; ++cy) {
 #pragma unroll
               for (int cx = 0; cx < CX; ++cx) {
-                double x;
+                E x;
                 if constexpr (plane_needs_inplane<SH>(o.d0))
                   x = ext[o.d0 + R][cy + o.d1 + R][cx + o.d2 + R];
                 else
                   x = win[s - 1][pmod<WN>(uu - s * Z + o.d0)][cy][cx];
                 if constexpr (UNI)
-                  acc[cy][cx] = (i == 0) ? x : __dadd_rn(acc[cy][cx], x);
+                  acc[cy][cx] = (i == 0) ? x : add_rn<E>(acc[cy][cx], x);
                 else if constexpr (i == 0)
                   acc[cy][cx] = tap_first<EXACT>(cf.c[0], x);
                 else
@@ -335,8 +337,8 @@ __device__ __forceinline__ int stream3d_unit(const CUtensorMap* tm, double* __re
             for (int cx = 0; cx < CX; ++cx) {
               // UNI: levels < T carry products; a frame cell's product never
               // changes, and level T skips frame cells (host pre-copies them)
-              const double val =
-                  (UNI && s < T) ? __dmul_rn(cf.c[0], acc[cy][cx]) : acc[cy][cx];
+              const E val =
+                  (UNI && s < T) ? mul_rn<E>(cf.c[0], acc[cy][cx]) : acc[cy][cx];
               if constexpr (EDGE || FPL) {
                 bool f = fpl;
                 if constexpr (EDGE) f = f || ((fmask >> (cy * CX + cx)) & 1u);
@@ -356,7 +358,7 @@ __device__ __forceinline__ int stream3d_unit(const CUtensorMap* tm, double* __re
           bool qok = (q >= r0) && (q < r1);
           if (UNI && FPL) qok = qok && !fpl;
           if (qok) {
-            double* o = obase + (long long)q * plane;
+            E* o = obase + (long long)q * plane;
 #pragma unroll
             for (int cy = 0; cy < CY; ++cy)
 #pragma unroll
@@ -401,18 +403,19 @@ __host__ __device__ constexpr bool ps_eligible() {
   return true;
 }
 
-template <class SH, int T, int CY, int CX, int NWY, int S, int FL, bool EXACT, bool UNI, bool EDGE>
-__device__ __forceinline__ int stream3d_unit_ps(const CUtensorMap* tm, double* __restrict__ out,
-                                                double* ring, double* halo, uint64_t* bars,
+template <class SH, int T, int CY, int CX, int NWY, int S, int FL, bool EXACT, bool UNI, bool EDGE,
+          class E>
+__device__ __forceinline__ int stream3d_unit_ps(const CUtensorMap* tm, E* __restrict__ out,
+                                                E* ring, E* halo, uint64_t* bars,
                                                 uint32_t ring_cnt, int warp, int lane, int n0,
                                                 int n1, int n2, int X0, int Y0, int xlo,
                                                 int xhi, int ylo, int yhi, int r0, int r1,
-                                                const Coefs<SH::NT>& cf) {
-  using Cfg = Stream3DCfg<SH, T, CY, CX, NWY, S, FL>;
+                                                const Coefs<SH::NT, E>& cf) {
+  using Cfg = Stream3DCfg<SH, T, CY, CX, NWY, S, FL, E>;
   static_assert(ps_eligible<SH>(), "partial-sum path needs a radius-1 star in catalog order");
   constexpr int NB = Cfg::NB;
   constexpr int LY = Cfg::LY, LX = Cfg::LX;
-  constexpr int PLANE_BYTES = LY * LX * 8;
+  constexpr int PLANE_BYTES = LY * LX * (int)sizeof(E);
   static_assert(Cfg::Z == 1 && NB >= 2, "star skew");
   static_assert(CY * CX <= 32, "cell masks are 32-bit");
 
@@ -450,7 +453,7 @@ __device__ __forceinline__ int stream3d_unit_ps(const CUtensorMap* tm, double* _
   // Y[s]: newest plane of level s; P[s]: partial sum (taps 0 and 1) of level
   // s+1's next target.  Level s+1 at advance k targets q = k-s-1, whose centre
   // is Y[s] (produced last advance) and whose z+1 plane is produced now.
-  double Y[T][CY][CX], P[T][CY][CX];
+  E Y[T][CY][CX], P[T][CY][CX];
 #pragma unroll
   for (int s = 0; s < T; ++s)
 #pragma unroll
@@ -458,41 +461,41 @@ __device__ __forceinline__ int stream3d_unit_ps(const CUtensorMap* tm, double* _
 #pragma unroll
       for (int cx = 0; cx < CX; ++cx) Y[s][cy][cx] = P[s][cy][cx] = 0.0;
 
-  auto hrow = [&](int level, int b, int w, int r) -> double* {
+  auto hrow = [&](int level, int b, int w, int r) -> E* {
     return halo + (size_t)(level * NB + b) * Cfg::HPLANE + (size_t)(w * 2 + r) * LX + tx0;
   };
-  auto push = [&](int level, int b, const double (&v)[CY][CX]) {
+  auto push = [&](int level, int b, const E (&v)[CY][CX]) {
 #pragma unroll
     for (int r = 0; r < 2; ++r) {
       const int cy = r == 0 ? 0 : CY - 1;
-      double* d = hrow(level, b, warp, r);
+      E* d = hrow(level, b, warp, r);
 #pragma unroll
       for (int cx = 0; cx < CX; cx += 2)
-        *reinterpret_cast<double2*>(d + cx) = make_double2(v[cy][cx], v[cy][cx + 1]);
+        *reinterpret_cast<vec2_t<E>*>(d + cx) = make_v2<E>(v[cy][cx], v[cy][cx + 1]);
     }
   };
   const int wa = warp > 0 ? warp - 1 : warp;
   const int wbl = warp < NWY - 1 ? warp + 1 : warp;
   const long long plane = (long long)n1 * (long long)n2;
-  double* obase = out + ((long long)(Y0 + ty0) * n2 + (X0 + tx0));
+  E* obase = out + ((long long)(Y0 + ty0) * n2 + (X0 + tx0));
 
   auto advance = [&](int k, auto fpl_tag) {
     constexpr bool FPL = decltype(fpl_tag)::value;
     const int bk = k & (NB - 1);        // halo buffer written this advance
     const int bp = (k - 1) & (NB - 1);  // centre planes were pushed last advance
-    double nw[CY][CX];                  // newest plane of the level below
+    E nw[CY][CX];                  // newest plane of the level below
     {
       const uint32_t pos = ring_cnt + (uint32_t)(k - ka);
       const uint32_t slot = pos & (S - 1);
       mbar_wait(&bars[slot], (pos / S) & 1);
-      const double* p = ring + slot * Cfg::RING_PLANE + ty0 * LX + tx0;
+      const E* p = ring + slot * Cfg::RING_PLANE + ty0 * LX + tx0;
 #pragma unroll
       for (int cy = 0; cy < CY; ++cy)
 #pragma unroll
         for (int cx = 0; cx < CX; cx += 2) {
-          const double2 t2 = *reinterpret_cast<const double2*>(p + cy * LX + cx);
-          nw[cy][cx] = UNI ? __dmul_rn(cf.c[0], t2.x) : t2.x;
-          nw[cy][cx + 1] = UNI ? __dmul_rn(cf.c[0], t2.y) : t2.y;
+          const vec2_t<E> t2 = *reinterpret_cast<const vec2_t<E>*>(p + cy * LX + cx);
+          nw[cy][cx] = UNI ? mul_rn<E>(cf.c[0], t2.x) : t2.x;
+          nw[cy][cx + 1] = UNI ? mul_rn<E>(cf.c[0], t2.y) : t2.y;
         }
       push(0, bk, nw);
     }
@@ -502,18 +505,18 @@ __device__ __forceinline__ int stream3d_unit_ps(const CUtensorMap* tm, double* _
       bool fpl = false;
       if constexpr (FPL) fpl = (q < 1) || (q >= n0 - 1);
       // centre plane of level s-1 with its in-plane halo
-      double ext[CY + 2][CX + 2];
+      E ext[CY + 2][CX + 2];
 #pragma unroll
       for (int cy = 0; cy < CY; ++cy)
 #pragma unroll
         for (int cx = 0; cx < CX; ++cx) ext[cy + 1][cx + 1] = Y[s - 1][cy][cx];
       {
-        const double* up = hrow(s - 1, bp, wa, warp > 0 ? 1 : 0);
-        const double* dn = hrow(s - 1, bp, wbl, warp < NWY - 1 ? 0 : 1);
+        const E* up = hrow(s - 1, bp, wa, warp > 0 ? 1 : 0);
+        const E* dn = hrow(s - 1, bp, wbl, warp < NWY - 1 ? 0 : 1);
 #pragma unroll
         for (int cx = 0; cx < CX; cx += 2) {
-          const double2 a2 = *reinterpret_cast<const double2*>(up + cx);
-          const double2 b2 = *reinterpret_cast<const double2*>(dn + cx);
+          const vec2_t<E> a2 = *reinterpret_cast<const vec2_t<E>*>(up + cx);
+          const vec2_t<E> b2 = *reinterpret_cast<const vec2_t<E>*>(dn + cx);
           ext[0][cx + 1] = a2.x;
           ext[0][cx + 2] = a2.y;
           ext[CY + 1][cx + 1] = b2.x;
@@ -525,26 +528,26 @@ __device__ __forceinline__ int stream3d_unit_ps(const CUtensorMap* tm, double* _
         ext[cy][0] = __shfl_up_sync(kFullMask, ext[cy][CX], 1);
         ext[cy][CX + 1] = __shfl_down_sync(kFullMask, ext[cy][1], 1);
       }
-      double nv[CY][CX];
+      E nv[CY][CX];
 #pragma unroll
       for (int cy = 0; cy < CY; ++cy)
 #pragma unroll
         for (int cx = 0; cx < CX; ++cx) {
-          double acc;
+          E acc;
           if constexpr (UNI)
-            acc = __dadd_rn(P[s - 1][cy][cx], nw[cy][cx]);
+            acc = add_rn<E>(P[s - 1][cy][cx], nw[cy][cx]);
           else
             acc = tap_next<EXACT>(P[s - 1][cy][cx], cf.c[2], nw[cy][cx]);
           static_for<SH::NT - 3>([&](auto iI) {
             constexpr int i = decltype(iI)::value + 3;
             constexpr Off o = SH::tap(i);
-            const double x = ext[cy + 1 + o.d1][cx + 1 + o.d2];
+            const E x = ext[cy + 1 + o.d1][cx + 1 + o.d2];
             if constexpr (UNI)
-              acc = __dadd_rn(acc, x);
+              acc = add_rn<E>(acc, x);
             else
               acc = tap_next<EXACT>(acc, cf.c[i], x);
           });
-          const double val = (UNI && s < T) ? __dmul_rn(cf.c[0], acc) : acc;
+          const E val = (UNI && s < T) ? mul_rn<E>(cf.c[0], acc) : acc;
           if constexpr (EDGE || FPL) {
             bool f = fpl;
             if constexpr (EDGE) f = f || ((fmask >> (cy * CX + cx)) & 1u);
@@ -559,7 +562,7 @@ __device__ __forceinline__ int stream3d_unit_ps(const CUtensorMap* tm, double* _
 #pragma unroll
         for (int cx = 0; cx < CX; ++cx) {
           if constexpr (UNI)
-            P[s - 1][cy][cx] = __dadd_rn(Y[s - 1][cy][cx], nw[cy][cx]);
+            P[s - 1][cy][cx] = add_rn<E>(Y[s - 1][cy][cx], nw[cy][cx]);
           else
             P[s - 1][cy][cx] = tap_next<EXACT>(tap_first<EXACT>(cf.c[0], Y[s - 1][cy][cx]),
                                                cf.c[1], nw[cy][cx]);
@@ -572,7 +575,7 @@ __device__ __forceinline__ int stream3d_unit_ps(const CUtensorMap* tm, double* _
         bool qok = (q >= r0) && (q < r1);
         if (UNI && FPL) qok = qok && !fpl;
         if (qok) {
-          double* o = obase + (long long)q * plane;
+          E* o = obase + (long long)q * plane;
 #pragma unroll
           for (int cy = 0; cy < CY; ++cy)
 #pragma unroll
@@ -618,21 +621,22 @@ __host__ __device__ constexpr bool pm_eligible() {
   return true;
 }
 
-template <class SH, int T, int CY, int CX, int NWY, int S, int FL, bool EXACT, bool UNI, bool EDGE>
-__device__ __forceinline__ int stream3d_unit_pm(const CUtensorMap* tm, double* __restrict__ out,
-                                                double* ring, double* halo, uint64_t* bars,
+template <class SH, int T, int CY, int CX, int NWY, int S, int FL, bool EXACT, bool UNI, bool EDGE,
+          class E>
+__device__ __forceinline__ int stream3d_unit_pm(const CUtensorMap* tm, E* __restrict__ out,
+                                                E* ring, E* halo, uint64_t* bars,
                                                 uint32_t ring_cnt, int warp, int lane, int n0,
                                                 int n1, int n2, int X0, int Y0, int xlo,
                                                 int xhi, int ylo, int yhi, int r0, int r1,
-                                                const Coefs<SH::NT>& cf) {
-  using Cfg = Stream3DCfg<SH, T, CY, CX, NWY, S, FL>;
+                                                const Coefs<SH::NT, E>& cf) {
+  using Cfg = Stream3DCfg<SH, T, CY, CX, NWY, S, FL, E>;
   static_assert(pm_eligible<SH>(), "plane-major path needs sorted radius-1 taps");
   constexpr int NB = Cfg::NB;
   constexpr int LY = Cfg::LY, LX = Cfg::LX;
-  constexpr int PLANE_BYTES = LY * LX * 8;
+  constexpr int PLANE_BYTES = LY * LX * (int)sizeof(E);
   static_assert(NB >= 2, "halo slots");
   static_assert(CY * CX <= 32, "cell masks are 32-bit");
-  static_assert(CX % 2 == 0, "double2 rows");
+  static_assert(CX % 2 == 0, "vec2_t<E> rows");
 
   const int ka = max(0, r0 - T);
   // level s emits plane k - 2s; advances in pairs (register sets alternate)
@@ -666,7 +670,7 @@ __device__ __forceinline__ int stream3d_unit_pm(const CUtensorMap* tm, double* _
   // per level s (1..T), index s-1:  A = target c+1 after its z-1 taps,
   // B = target c after its z-1 and z taps, Yc = the level-below plane to
   // consume next advance, Yp = the one consumed last (frame carry)
-  double A[T][CY][CX], B[T][CY][CX], Yc[T][CY][CX], Yp[T][CY][CX];
+  E A[T][CY][CX], B[T][CY][CX], Yc[T][CY][CX], Yp[T][CY][CX];
 #pragma unroll
   for (int s = 0; s < T; ++s)
 #pragma unroll
@@ -674,38 +678,38 @@ __device__ __forceinline__ int stream3d_unit_pm(const CUtensorMap* tm, double* _
 #pragma unroll
       for (int cx = 0; cx < CX; ++cx) A[s][cy][cx] = B[s][cy][cx] = Yc[s][cy][cx] = Yp[s][cy][cx] = 0.0;
 
-  auto hrow = [&](int level, int b, int w, int r) -> double* {
+  auto hrow = [&](int level, int b, int w, int r) -> E* {
     return halo + (size_t)(level * NB + b) * Cfg::HPLANE + (size_t)(w * 2 + r) * LX + tx0;
   };
-  auto push = [&](int level, int b, const double (&v)[CY][CX]) {
+  auto push = [&](int level, int b, const E (&v)[CY][CX]) {
 #pragma unroll
     for (int r = 0; r < 2; ++r) {
       const int cy = r == 0 ? 0 : CY - 1;
-      double* d = hrow(level, b, warp, r);
+      E* d = hrow(level, b, warp, r);
 #pragma unroll
       for (int cx = 0; cx < CX; cx += 2)
-        *reinterpret_cast<double2*>(d + cx) = make_double2(v[cy][cx], v[cy][cx + 1]);
+        *reinterpret_cast<vec2_t<E>*>(d + cx) = make_v2<E>(v[cy][cx], v[cy][cx + 1]);
     }
   };
   const int wa = warp > 0 ? warp - 1 : warp;
   const int wbl = warp < NWY - 1 ? warp + 1 : warp;
   const long long plane = (long long)n1 * (long long)n2;
-  double* obase = out + ((long long)(Y0 + ty0) * n2 + (X0 + tx0));
+  E* obase = out + ((long long)(Y0 + ty0) * n2 + (X0 + tx0));
 
   // sum of the taps with axis-0 offset DZ over the gathered neighbourhood,
   // starting from `acc` (FIRST: the run opens the target's sum)
-  auto run_taps = [&](auto dz_tag, auto first_tag, const double (&e)[CY + 2][CX + 2], int cy,
-                      int cx, double acc) -> double {
+  auto run_taps = [&](auto dz_tag, auto first_tag, const E (&e)[CY + 2][CX + 2], int cy,
+                      int cx, E acc) -> E {
     constexpr int DZ = decltype(dz_tag)::value;
     constexpr bool FIRST = decltype(first_tag)::value;
     static_for<SH::NT>([&](auto iI) {
       constexpr int i = decltype(iI)::value;
       constexpr Off o = SH::tap(i);
       if constexpr (o.d0 == DZ) {
-        const double x = e[cy + 1 + o.d1][cx + 1 + o.d2];
+        const E x = e[cy + 1 + o.d1][cx + 1 + o.d2];
         constexpr bool OPEN = FIRST && (i == 0 || SH::tap(i > 0 ? i - 1 : 0).d0 != DZ);
         if constexpr (UNI)
-          acc = OPEN ? x : __dadd_rn(acc, x);
+          acc = OPEN ? x : add_rn<E>(acc, x);
         else if constexpr (OPEN)
           acc = tap_first<EXACT>(cf.c[i], x);
         else
@@ -719,19 +723,19 @@ __device__ __forceinline__ int stream3d_unit_pm(const CUtensorMap* tm, double* _
     constexpr bool FPL = decltype(fpl_tag)::value;
     const int bk = k & (NB - 1);
     const int bp = (k - 1) & (NB - 1);
-    double nw[CY][CX];  // newest plane of the level below (produced this advance)
+    E nw[CY][CX];  // newest plane of the level below (produced this advance)
     {
       const uint32_t pos = ring_cnt + (uint32_t)(k - ka);
       const uint32_t slot = pos & (S - 1);
       mbar_wait(&bars[slot], (pos / S) & 1);
-      const double* p = ring + slot * Cfg::RING_PLANE + ty0 * LX + tx0;
+      const E* p = ring + slot * Cfg::RING_PLANE + ty0 * LX + tx0;
 #pragma unroll
       for (int cy = 0; cy < CY; ++cy)
 #pragma unroll
         for (int cx = 0; cx < CX; cx += 2) {
-          const double2 t2 = *reinterpret_cast<const double2*>(p + cy * LX + cx);
-          nw[cy][cx] = UNI ? __dmul_rn(cf.c[0], t2.x) : t2.x;
-          nw[cy][cx + 1] = UNI ? __dmul_rn(cf.c[0], t2.y) : t2.y;
+          const vec2_t<E> t2 = *reinterpret_cast<const vec2_t<E>*>(p + cy * LX + cx);
+          nw[cy][cx] = UNI ? mul_rn<E>(cf.c[0], t2.x) : t2.x;
+          nw[cy][cx + 1] = UNI ? mul_rn<E>(cf.c[0], t2.y) : t2.y;
         }
       push(0, bk, nw);
     }
@@ -741,18 +745,18 @@ __device__ __forceinline__ int stream3d_unit_pm(const CUtensorMap* tm, double* _
       bool fpl = false;
       if constexpr (FPL) fpl = (q < 1) || (q >= n0 - 1);
       // gather the consumed plane (level s-1, produced last advance) once
-      double e[CY + 2][CX + 2];
+      E e[CY + 2][CX + 2];
 #pragma unroll
       for (int cy = 0; cy < CY; ++cy)
 #pragma unroll
         for (int cx = 0; cx < CX; ++cx) e[cy + 1][cx + 1] = Yc[s - 1][cy][cx];
       {
-        const double* up = hrow(s - 1, bp, wa, warp > 0 ? 1 : 0);
-        const double* dn = hrow(s - 1, bp, wbl, warp < NWY - 1 ? 0 : 1);
+        const E* up = hrow(s - 1, bp, wa, warp > 0 ? 1 : 0);
+        const E* dn = hrow(s - 1, bp, wbl, warp < NWY - 1 ? 0 : 1);
 #pragma unroll
         for (int cx = 0; cx < CX; cx += 2) {
-          const double2 a2 = *reinterpret_cast<const double2*>(up + cx);
-          const double2 b2 = *reinterpret_cast<const double2*>(dn + cx);
+          const vec2_t<E> a2 = *reinterpret_cast<const vec2_t<E>*>(up + cx);
+          const vec2_t<E> b2 = *reinterpret_cast<const vec2_t<E>*>(dn + cx);
           e[0][cx + 1] = a2.x;
           e[0][cx + 2] = a2.y;
           e[CY + 1][cx + 1] = b2.x;
@@ -764,18 +768,18 @@ __device__ __forceinline__ int stream3d_unit_pm(const CUtensorMap* tm, double* _
         e[ey][0] = __shfl_up_sync(kFullMask, e[ey][CX], 1);
         e[ey][CX + 1] = __shfl_down_sync(kFullMask, e[ey][1], 1);
       }
-      double nv[CY][CX];
+      E nv[CY][CX];
 #pragma unroll
       for (int cy = 0; cy < CY; ++cy)
 #pragma unroll
         for (int cx = 0; cx < CX; ++cx) {
-          const double C = run_taps(std::integral_constant<int, 1>{}, std::false_type{}, e, cy,
+          const E C = run_taps(std::integral_constant<int, 1>{}, std::false_type{}, e, cy,
                                     cx, B[s - 1][cy][cx]);
-          const double Bn = run_taps(std::integral_constant<int, 0>{}, std::false_type{}, e,
+          const E Bn = run_taps(std::integral_constant<int, 0>{}, std::false_type{}, e,
                                      cy, cx, A[s - 1][cy][cx]);
-          const double An = run_taps(std::integral_constant<int, -1>{}, std::true_type{}, e, cy,
+          const E An = run_taps(std::integral_constant<int, -1>{}, std::true_type{}, e, cy,
                                      cx, 0.0);
-          const double val = (UNI && s < T) ? __dmul_rn(cf.c[0], C) : C;
+          const E val = (UNI && s < T) ? mul_rn<E>(cf.c[0], C) : C;
           if constexpr (EDGE || FPL) {
             bool f = fpl;
             if constexpr (EDGE) f = f || ((fmask >> (cy * CX + cx)) & 1u);
@@ -795,7 +799,7 @@ __device__ __forceinline__ int stream3d_unit_pm(const CUtensorMap* tm, double* _
         bool qok = (q >= r0) && (q < r1);
         if (UNI && FPL) qok = qok && !fpl;
         if (qok) {
-          double* o = obase + (long long)q * plane;
+          E* o = obase + (long long)q * plane;
 #pragma unroll
           for (int cy = 0; cy < CY; ++cy)
 #pragma unroll
@@ -825,15 +829,16 @@ __device__ __forceinline__ int stream3d_unit_pm(const CUtensorMap* tm, double* _
   return nadv;
 }
 
-template <class SH, int T, int CY, int CX, int NWY, int S, int FL, bool EXACT, bool UNI, int MINB>
+template <class SH, int T, int CY, int CX, int NWY, int S, int FL, bool EXACT, bool UNI, int MINB,
+          class E = double>
 __global__ void __launch_bounds__(NWY * 32, MINB)
     k_stream3d(const __grid_constant__ TmapSet maps, const Stream3DArgs a,
-               const __grid_constant__ Coefs<SH::NT> cf) {
-  using Cfg = Stream3DCfg<SH, T, CY, CX, NWY, S, FL>;
+               const __grid_constant__ Coefs<SH::NT, E> cf) {
+  using Cfg = Stream3DCfg<SH, T, CY, CX, NWY, S, FL, E>;
   constexpr int R = Cfg::R;
   extern __shared__ __align__(1024) unsigned char smem[];
-  double* ring = reinterpret_cast<double*>(smem);
-  double* halo = reinterpret_cast<double*>(smem + Cfg::RING_BYTES);
+  E* ring = reinterpret_cast<E*>(smem);
+  E* halo = reinterpret_cast<E*>(smem + Cfg::RING_BYTES);
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem + Cfg::RING_BYTES + Cfg::HALO_BYTES);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
 
@@ -854,7 +859,7 @@ __global__ void __launch_bounds__(NWY * 32, MINB)
   int src = a.first_src, dst = a.first_dst;
   for (int e = 0; e < a.epochs; ++e) {
     const CUtensorMap* tm = &maps.m[src];
-    double* __restrict__ out = (dst == BUF_OUT) ? a.buf[BUF_OUT] : a.buf[BUF_SCR];
+    E* __restrict__ out = static_cast<E*>((dst == BUF_OUT) ? a.buf[BUF_OUT] : a.buf[BUF_SCR]);
     __shared__ int s_unit;
     for (;;) {
       // dynamic unit distribution across CTAs (tail <= one unit)
@@ -882,25 +887,25 @@ __global__ void __launch_bounds__(NWY * 32, MINB)
       int used;
       if constexpr (pm_eligible<SH>() && (FL & 1) == 0) {
         if (edge)
-          used = stream3d_unit_pm<SH, T, CY, CX, NWY, S, FL, EXACT, UNI, true>(
+          used = stream3d_unit_pm<SH, T, CY, CX, NWY, S, FL, EXACT, UNI, true, E>(
               tm, out, ring, halo, bars, ring_cnt, warp, lane, n0, n1, n2, X0, Y0, gx.vlo, gx.vhi,
               gy.vlo, gy.vhi, r0, r1, cf);
         else
-          used = stream3d_unit_pm<SH, T, CY, CX, NWY, S, FL, EXACT, UNI, false>(
+          used = stream3d_unit_pm<SH, T, CY, CX, NWY, S, FL, EXACT, UNI, false, E>(
               tm, out, ring, halo, bars, ring_cnt, warp, lane, n0, n1, n2, X0, Y0, gx.vlo, gx.vhi,
               gy.vlo, gy.vhi, r0, r1, cf);
       } else if constexpr (ps_eligible<SH>() && (FL & 1) == 0) {
         if (edge)
-          used = stream3d_unit_ps<SH, T, CY, CX, NWY, S, FL, EXACT, UNI, true>(
+          used = stream3d_unit_ps<SH, T, CY, CX, NWY, S, FL, EXACT, UNI, true, E>(
               tm, out, ring, halo, bars, ring_cnt, warp, lane, n0, n1, n2, X0, Y0, gx.vlo, gx.vhi, gy.vlo, gy.vhi, r0, r1, cf);
         else
-          used = stream3d_unit_ps<SH, T, CY, CX, NWY, S, FL, EXACT, UNI, false>(
+          used = stream3d_unit_ps<SH, T, CY, CX, NWY, S, FL, EXACT, UNI, false, E>(
               tm, out, ring, halo, bars, ring_cnt, warp, lane, n0, n1, n2, X0, Y0, gx.vlo, gx.vhi, gy.vlo, gy.vhi, r0, r1, cf);
       } else if (edge)
-        used = stream3d_unit<SH, T, CY, CX, NWY, S, FL, EXACT, UNI, true>(
+        used = stream3d_unit<SH, T, CY, CX, NWY, S, FL, EXACT, UNI, true, E>(
             tm, out, ring, halo, bars, ring_cnt, warp, lane, n0, n1, n2, X0, Y0, gx.vlo, gx.vhi, gy.vlo, gy.vhi, r0, r1, cf);
       else
-        used = stream3d_unit<SH, T, CY, CX, NWY, S, FL, EXACT, UNI, false>(
+        used = stream3d_unit<SH, T, CY, CX, NWY, S, FL, EXACT, UNI, false, E>(
             tm, out, ring, halo, bars, ring_cnt, warp, lane, n0, n1, n2, X0, Y0, gx.vlo, gx.vhi, gy.vlo, gy.vhi, r0, r1, cf);
       ring_cnt += (uint32_t)used;
       __syncthreads();  // halo buffers and s_unit are reused by the next unit

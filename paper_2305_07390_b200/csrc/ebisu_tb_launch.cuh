@@ -11,10 +11,10 @@
 
 namespace ebisu {
 
-template <class SH, int T, int C, int NW, int S, bool EXACT, bool UNI, int MINB>
+template <class SH, int T, int C, int NW, int S, bool EXACT, bool UNI, int MINB, class E>
 cudaError_t launch_stream2d(const TbLaunch& L) {
-  using Cfg = Stream2DCfg<SH, T, C, NW, S>;
-  auto kern = k_stream2d<SH, T, C, NW, S, EXACT, UNI, MINB>;
+  using Cfg = Stream2DCfg<SH, T, C, NW, S, E>;
+  auto kern = k_stream2d<SH, T, C, NW, S, EXACT, UNI, MINB, E>;
   cudaError_t err =
       cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg::SMEM_BYTES);
   if (err != cudaSuccess) return err;
@@ -37,8 +37,8 @@ cudaError_t launch_stream2d(const TbLaunch& L) {
   for (int i = 0; i < 3; ++i) a.buf[i] = L.buf[i];
   a.unit_clock = L.unit_clock;
   a.work = L.work;
-  Coefs<SH::NT> cf;
-  for (int i = 0; i < SH::NT; ++i) cf.c[i] = L.coeffs[i];
+  Coefs<SH::NT, E> cf;
+  for (int i = 0; i < SH::NT; ++i) cf.c[i] = (E)L.coeffs[i];
   if (L.cooperative) {
     void* args[] = {(void*)&maps, (void*)&a, (void*)&cf};
     return cudaLaunchCooperativeKernel((const void*)kern, dim3(L.grid), dim3(NW * 32), args,
@@ -54,25 +54,28 @@ cudaError_t launch_stream2d(const TbLaunch& L) {
 #ifndef EBISU_MINB_BIAS
 #define EBISU_MINB_BIAS 0
 #endif
-constexpr int s2d_minb(int T, int R, int C, int NW) {
-  const int est = 2 * T * (2 * R + 1) * C + 64;
+constexpr int s2d_minb(int T, int R, int C, int NW, int ebytes = 8) {
+  const int est = ebytes / 4 * T * (2 * R + 1) * C + 64;
   int m = 65536 / (NW * 32 * (est < 64 ? 64 : est)) + EBISU_MINB_BIAS;
   return m < 1 ? 1 : (m > 8 ? 8 : m);
 }
 
-#define EBISU_S2D_ENTRY(SHAPE_ID, SH, T, C, NW, S, EX, UNI)                                    \
+#define EBISU_S2D_ENTRY(SHAPE_ID, SH, T, C, NW, S, EX, UNI, E)                                 \
   TbKernel {                                                                                  \
-    SHAPE_ID, 2, T, C, NW, S, EX, UNI, Stream2DCfg<SH, T, C, NW, S>::SMEM_BYTES, 32 * C, 1, 1, \
-        Stream2DCfg<SH, T, C, NW, S>::VW, 0, 0, 0,                                            \
+    SHAPE_ID, 2, T, C, NW, S, EX, UNI, Stream2DCfg<SH, T, C, NW, S, E>::SMEM_BYTES, 32 * C, 1, \
+        1, Stream2DCfg<SH, T, C, NW, S, E>::VW, 0, 0, 0,                                     \
         (const void*)&k_stream2d<SH, T, C, NW, S, (EX) != 0, (UNI) != 0,                      \
-                                 s2d_minb(T, SH::R, C, NW)>,                                  \
-        &launch_stream2d<SH, T, C, NW, S, (EX) != 0, (UNI) != 0, s2d_minb(T, SH::R, C, NW)>   \
+                                 s2d_minb(T, SH::R, C, NW, (int)sizeof(E)), E>,               \
+        &launch_stream2d<SH, T, C, NW, S, (EX) != 0, (UNI) != 0,                              \
+                         s2d_minb(T, SH::R, C, NW, (int)sizeof(E)), E>,                       \
+        0, (int)sizeof(E)                                                                     \
   }
 
-template <class SH, int T, int CY, int CX, int NWY, int S, int FL, bool EXACT, bool UNI, int MINB>
+template <class SH, int T, int CY, int CX, int NWY, int S, int FL, bool EXACT, bool UNI, int MINB,
+          class E>
 cudaError_t launch_stream3d(const TbLaunch& L) {
-  using Cfg = Stream3DCfg<SH, T, CY, CX, NWY, S, FL>;
-  auto kern = k_stream3d<SH, T, CY, CX, NWY, S, FL, EXACT, UNI, MINB>;
+  using Cfg = Stream3DCfg<SH, T, CY, CX, NWY, S, FL, E>;
+  auto kern = k_stream3d<SH, T, CY, CX, NWY, S, FL, EXACT, UNI, MINB, E>;
   cudaError_t err =
       cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg::SMEM_BYTES);
   if (err != cudaSuccess) return err;
@@ -97,8 +100,8 @@ cudaError_t launch_stream3d(const TbLaunch& L) {
   a.first_dst = L.first_dst;
   for (int i = 0; i < 3; ++i) a.buf[i] = L.buf[i];
   a.work = L.work;
-  Coefs<SH::NT> cf;
-  for (int i = 0; i < SH::NT; ++i) cf.c[i] = L.coeffs[i];
+  Coefs<SH::NT, E> cf;
+  for (int i = 0; i < SH::NT; ++i) cf.c[i] = (E)L.coeffs[i];
   if (L.cooperative) {
     void* args[] = {(void*)&maps, (void*)&a, (void*)&cf};
     return cudaLaunchCooperativeKernel((const void*)kern, dim3(L.grid), dim3(NWY * 32), args,
@@ -108,16 +111,20 @@ cudaError_t launch_stream3d(const TbLaunch& L) {
   return cudaGetLastError();
 }
 
-#define EBISU_S3D_ENTRY(SHAPE_ID, SH, T, CY, CX, NWY, S, FL, EX, UNI, MINB)                    \
+#define EBISU_S3D_ENTRY(SHAPE_ID, SH, T, CY, CX, NWY, S, FL, EX, UNI, MINB, E)                 \
   TbKernel {                                                                                  \
-    SHAPE_ID, 3, T, CX, NWY, S, EX, UNI, Stream3DCfg<SH, T, CY, CX, NWY, S, FL>::SMEM_BYTES,  \
-        Stream3DCfg<SH, T, CY, CX, NWY, S, FL>::LX, Stream3DCfg<SH, T, CY, CX, NWY, S, FL>::LY, \
-        1, Stream3DCfg<SH, T, CY, CX, NWY, S, FL>::VX,                                        \
-        Stream3DCfg<SH, T, CY, CX, NWY, S, FL>::VY, Stream3DCfg<SH, T, CY, CX, NWY, S, FL>::Z,  \
+    SHAPE_ID, 3, T, CX, NWY, S, EX, UNI, Stream3DCfg<SH, T, CY, CX, NWY, S, FL, E>::SMEM_BYTES, \
+        Stream3DCfg<SH, T, CY, CX, NWY, S, FL, E>::LX,                                        \
+        Stream3DCfg<SH, T, CY, CX, NWY, S, FL, E>::LY, 1,                                     \
+        Stream3DCfg<SH, T, CY, CX, NWY, S, FL, E>::VX,                                        \
+        Stream3DCfg<SH, T, CY, CX, NWY, S, FL, E>::VY,                                        \
+        Stream3DCfg<SH, T, CY, CX, NWY, S, FL, E>::Z,                                         \
         ((ps_eligible<SH>() || pm_eligible<SH>()) && ((FL) & 1) == 0)                        \
-            ? 2 : Stream3DCfg<SH, T, CY, CX, NWY, S, FL>::WN,                                  \
-        (const void*)&k_stream3d<SH, T, CY, CX, NWY, S, FL, (EX) != 0, (UNI) != 0, MINB>,    \
-        &launch_stream3d<SH, T, CY, CX, NWY, S, FL, (EX) != 0, (UNI) != 0, MINB>             \
+            ? 2                                                                               \
+            : Stream3DCfg<SH, T, CY, CX, NWY, S, FL, E>::WN,                                  \
+        (const void*)&k_stream3d<SH, T, CY, CX, NWY, S, FL, (EX) != 0, (UNI) != 0, MINB, E>,  \
+        &launch_stream3d<SH, T, CY, CX, NWY, S, FL, (EX) != 0, (UNI) != 0, MINB, E>, 0,      \
+        (int)sizeof(E)                                                                        \
   }
 
 template <class SH, int T, int C, int NW, int S, bool EXACT, bool UNI, int MINB>
@@ -141,7 +148,7 @@ cudaError_t launch_halo2d(const TbLaunch& L) {
   a.first_src = L.first_src;
   a.first_dst = L.first_dst;
   a.aligned = L.aligned;
-  for (int i = 0; i < 3; ++i) a.buf[i] = L.buf[i];
+  for (int i = 0; i < 3; ++i) a.buf[i] = static_cast<double*>(L.buf[i]);
   a.work = L.work;
   Coefs<SH::NT> cf;
   for (int i = 0; i < SH::NT; ++i) cf.c[i] = L.coeffs[i];
@@ -162,7 +169,7 @@ cudaError_t launch_halo2d(const TbLaunch& L) {
         Halo2DCfg<SH, T, C, NW, S>::VW, 0, Halo2DCfg<SH, T, C, NW, S>::Z,                     \
         Halo2DCfg<SH, T, C, NW, S>::LW,                                                       \
         (const void*)&k_halo2d<SH, T, C, NW, S, (EX) != 0, (UNI) != 0, MINB>,                 \
-        &launch_halo2d<SH, T, C, NW, S, (EX) != 0, (UNI) != 0, MINB>, 1                      \
+        &launch_halo2d<SH, T, C, NW, S, (EX) != 0, (UNI) != 0, MINB>, 1, 8                   \
   }
 
 }  // namespace ebisu

@@ -25,11 +25,12 @@ def _stream_ptr(stream=None) -> int:
     return int(s.cuda_stream)
 
 
-def _check_tensor(x, name):
+def _check_tensor(x, name, dtype=None):
     torch = _torch()
-    if not (isinstance(x, torch.Tensor) and x.is_cuda and x.dtype == torch.float64
+    dtype = dtype or torch.float64
+    if not (isinstance(x, torch.Tensor) and x.is_cuda and x.dtype == dtype
             and x.is_contiguous()):
-        raise ValueError(f"{name} must be a contiguous float64 CUDA tensor")
+        raise ValueError(f"{name} must be a contiguous {str(dtype).split('.')[-1]} CUDA tensor")
 
 
 def empty_grid(extents, device="cuda"):
@@ -53,10 +54,18 @@ def sweep_device(d_in, stencil: StencilShape, steps: int, *, out=None, scratch=N
                  persistent: bool = True, stream=None, trace: bool = False, params=None):
     """``steps`` Jacobi steps of the device grid ``d_in`` into ``out``.
 
+    float64 tensors run the reference arithmetic (bitwise in exact mode);
+    float32 tensors run the fp32 kernels (north-star tolerance 1e-5).
+
     Asynchronous on ``stream`` unless ``trace=True`` (then the call waits and
     returns the native counters with the device-measured ``elapsed_ms``).
     """
-    _check_tensor(d_in, "d_in")
+    torch = _torch()
+    if isinstance(d_in, torch.Tensor) and d_in.dtype == torch.float32:
+        dtype, run = torch.float32, "ebisu_run_device_f32"  # north-star 1e-5 mode
+    else:
+        dtype, run = torch.float64, "ebisu_run_device"
+    _check_tensor(d_in, "d_in", dtype)
     if steps < 0:
         raise ValueError("step count must be >= 0")
     if d_in.dim() != stencil.dims:
@@ -64,15 +73,15 @@ def sweep_device(d_in, stencil: StencilShape, steps: int, *, out=None, scratch=N
     lib = _native.load()
     if out is None:
         out = _torch().empty_like(d_in)
-    _check_tensor(out, "out")
+    _check_tensor(out, "out", dtype)
     if scratch is not None:
-        _check_tensor(scratch, "scratch")
+        _check_tensor(scratch, "scratch", dtype)
     st = _native.StencilArgs(stencil)
     ext = _native.extents_c(tuple(d_in.shape))
     prm = params if params is not None else _native.make_params(
         scheme=scheme, t=t, exact=exact, persistent=persistent)
     tr = _native.TraceC() if trace else None
-    rc = lib.ebisu_run_device(ctypes.byref(st.c), d_in.dim(), ext, d_in.data_ptr(),
+    rc = getattr(lib, run)(ctypes.byref(st.c), d_in.dim(), ext, d_in.data_ptr(),
                               out.data_ptr(), scratch.data_ptr() if scratch is not None else None,
                               int(steps), ctypes.byref(prm), _stream_ptr(stream),
                               ctypes.byref(tr) if tr is not None else None)

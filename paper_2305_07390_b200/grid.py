@@ -89,12 +89,15 @@ def _raise_native(rc: int, exc_param=None):
 
 def sweep(grid: Grid, stencil: StencilShape, steps: int, *, t: int = 0,
           scheme: int = _native.SCHEME_AUTO, exact: bool = True, persistent: bool = True,
-          trace: bool = False, params=None, exc_param=None):
+          trace: bool = False, params=None, exc_param=None, dtype=np.float64):
     """``steps`` Jacobi steps of ``grid`` on the GPU; returns ``Grid`` (and the
     native trace dict when ``trace=True``).
 
     ``t`` is the temporal depth fused per HBM round trip (0 = planner
     default).  Host buffers go through ``ebisu_run_host`` (H2D, sweep, D2H).
+    ``dtype=np.float32`` runs the fp32 kernels (``ebisu_run_host_f32``; the
+    north-star 1e-5 mode); the returned ``Grid`` holds those values as float64,
+    the reference Grid's type (grid.py:38).
     """
     if steps < 0:
         raise ValueError("step count must be >= 0")
@@ -103,15 +106,19 @@ def sweep(grid: Grid, stencil: StencilShape, steps: int, *, t: int = 0,
         out = grid.copy()
         return (out, None) if trace else out
     lib = _native.load()
-    src = np.ascontiguousarray(grid.cells, dtype=np.float64)
+    f32 = np.dtype(dtype) == np.float32
+    if not f32 and np.dtype(dtype) != np.float64:
+        raise ValueError("dtype must be float64 or float32")
+    src = np.ascontiguousarray(grid.cells, dtype=np.float32 if f32 else np.float64)
     dst = np.empty_like(src)
     st = _native.StencilArgs(stencil)
     ext = _native.extents_c(src.shape)
     prm = params if params is not None else _native.make_params(
         scheme=scheme, t=t, exact=exact, persistent=persistent)
     tr = _native.TraceC()
-    rc = lib.ebisu_run_host(ctypes.byref(st.c), src.ndim, ext, src.ctypes.data,
-                            dst.ctypes.data, int(steps), ctypes.byref(prm), ctypes.byref(tr))
+    run = lib.ebisu_run_host_f32 if f32 else lib.ebisu_run_host
+    rc = run(ctypes.byref(st.c), src.ndim, ext, src.ctypes.data, dst.ctypes.data, int(steps),
+             ctypes.byref(prm), ctypes.byref(tr))
     if rc != _native.EBISU_OK:
         _raise_native(rc, exc_param)
     out = Grid(dst, grid.boundary)

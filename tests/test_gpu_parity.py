@@ -388,3 +388,59 @@ def test_output_plane_range(name, ext, t, scheme):
         device.sweep_device(d_in, st, 2 * t + 1, out=split,
                             params=_native.make_params(t=t, out_planes=(0, cut)))
 
+
+
+FP32_RTOL = 1e-5  # north_star: fp32 outputs within 1e-5 of the fp64 reference
+
+
+@pytest.mark.parametrize("name", ["j2d5pt", "j2d9pt-gol", "j2d9pt", "j2d25pt", "j2d13pt",
+                                  "j2ds25pt", "j3d7pt", "j3d13pt", "j3d17pt", "j3d27pt",
+                                  "poisson", "j1d3pt"])
+def test_fp32_within_tolerance(name):
+    """fp32 kernels (ebisu_run_host_f32) against the fp64 oracle: relative
+    error <= 1e-5 of max |ref| on ragged grids at every fp32 depth, the fast
+    path (last extent a multiple of 4) and the naive fallback (odd extent)."""
+    st = _shape(name)
+    r = st.radius
+    rng = eb.SplitMix64(0xF32 + len(name))
+    # depths with an fp32 kernel at or below them (gen_instances.F32_2D/3D)
+    depths = {"j2d5pt": (4, 8, 12, 16), "j3d7pt": (2, 3, 4)}.get(
+        name, (1,) if st.dims == 1 else ((2, 3) if st.dims == 2 and r < 6 else (1, 2)))
+    for t in depths:
+        if st.dims == 1:
+            ext = (301,)
+        elif st.dims == 2:
+            ext = (2 * r + 1 + rng.randint(0, 300), 4 * (r + 1 + rng.randint(0, 300) // 4))
+        else:
+            ext = (2 * r + 1 + rng.randint(0, 40), 2 * r + 1 + rng.randint(0, 60),
+                   4 * (r + 1 + rng.randint(0, 60) // 4))
+        steps = rng.randint(t, 3 * t + 2)
+        g = eb.random_grid(ext, rng.next_u64())
+        ref = oracle_run(g.cells, taps_of(st), steps)
+        out, tr = eb.sweep(g, st, steps, t=t, trace=True, dtype=np.float32)
+        if st.dims >= 2:
+            assert tr["kernel"] in ("stream2d_tb", "stream3d_tb"), (name, t, tr["kernel"])
+        err = np.max(np.abs(out.cells - ref))
+        assert err <= FP32_RTOL * np.max(np.abs(ref)), (name, t, ext, steps, err)
+    # odd last extent: the fp32 naive kernel
+    ext = (2 * r + 9,) * (st.dims - 1) + (2 * r + 7,)
+    g = eb.random_grid(ext, 3)
+    out, tr = eb.sweep(g, st, 5, trace=True, dtype=np.float32)
+    ref = oracle_run(g.cells, taps_of(st), 5)
+    assert np.max(np.abs(out.cells - ref)) <= FP32_RTOL * np.max(np.abs(ref))
+
+
+def test_fp32_full_size_against_fp64_gpu():
+    """BASELINE config 2 geometry in fp32 (8192^2, 100 steps) against the fp64
+    GPU sweep, which is bitwise equal to the oracle (test_full_size_8192)."""
+    from paper_2305_07390_b200 import device
+
+    torch = _torch()
+    st = eb.make_benchmark("j2d5pt")
+    d64 = device.random_grid_device((8192, 8192), seed=1)
+    ref = device.sweep_device(d64, st, 100)
+    d32 = d64.float()
+    out, tr = device.sweep_device(d32, st, 100, trace=True)
+    assert out.dtype == torch.float32 and tr["kernel"] == "stream2d_tb"
+    err = (out.double() - ref).abs().max().item()
+    assert err <= FP32_RTOL * ref.abs().max().item(), err
