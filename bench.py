@@ -244,7 +244,16 @@ def extra_configs(eb, device, _native, torch, stream, hbm_peak):
     st27 = eb.make_benchmark("j3d27pt")
     tr = _timed_sweep(device, torch, d3, st27, 500, o3, s3)
     rec("config4_j3d27pt_512", st27, ext3, 500, tr)
+    d3f = d3.float()
     del d3, o3, s3
+    torch.cuda.empty_cache()
+    o3f = torch.empty_like(d3f)
+    s3f = torch.empty_like(d3f)
+    tr = _timed_sweep(device, torch, d3f, st3, 500, o3f, s3f)
+    rec("config4_j3d7pt_512_fp32", st3, ext3, 500, tr, dtype="f32")
+    out["config4_j3d7pt_512_fp32"]["naive_roofline_frac"] = round(
+        8 * out["config4_j3d7pt_512_fp32"]["value"] / hbm_peak, 3)
+    del d3f, o3f, s3f
     torch.cuda.empty_cache()
 
     # ---- config 3: large halos at 8192^2, overlapped vs halo exchange -------
@@ -262,8 +271,18 @@ def extra_configs(eb, device, _native, torch, stream, hbm_peak):
                 if best is None or tr["elapsed_ms"] < best["elapsed_ms"]:
                     best = tr
             rec(f"config3_{name}_8192_{tag}", st, ext2, 96, best, scheme=tag)
-    # naive yardstick: one launch per time step
+    # fp32 mode (north-star 1e-5 tolerance): configs 2 and 4 in binary32;
+    # the naive roofline is then 8 B per cell-step
     st5 = eb.make_benchmark("j2d5pt")
+    d2f = d2.float()
+    o2f = torch.empty_like(d2f)
+    s2f = torch.empty_like(d2f)
+    tr = _timed_sweep(device, torch, d2f, st5, 1000, o2f, s2f)
+    rec("config2_j2d5pt_8192_fp32", st5, ext2, 1000, tr, dtype="f32")
+    out["config2_j2d5pt_8192_fp32"]["naive_roofline_frac"] = round(
+        8 * out["config2_j2d5pt_8192_fp32"]["value"] / hbm_peak, 3)
+    del d2f, o2f, s2f
+    # naive yardstick: one launch per time step
     tr = _timed_sweep(device, torch, d2, st5, 20, o2, s2, scheme=_native.SCHEME_NAIVE)
     rec("naive_j2d5pt_8192", st5, ext2, 20, tr)
     del d2, o2, s2

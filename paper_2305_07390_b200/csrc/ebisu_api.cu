@@ -733,6 +733,8 @@ int run_device_impl(const ProblemDesc& p0, const void* d_in, void* d_out, void* 
                (!d_scr || reinterpret_cast<uintptr_t>(d_scr) % 16 == 0);
   if (tb_ok) {
     int t = (prm && prm->t > 0) ? prm->t : default_depth(p.shape_id);
+    // fp32 windows cost half the registers: the 2-D star runs deeper
+    if (!(prm && prm->t > 0) && p.elem == 4 && p.shape_id == SHAPE_J2D5PT) t = 16;
     const int want_c = prm ? prm->lane_cells : 0;
     const int want_v = prm ? prm->variant : 0;
     int fam = pick_family(scheme, p.shape_id, D);

@@ -10,7 +10,7 @@ Writes
   profiles/r01_ptb_model.json   the reference's own model (model.py:89-113,
                                 choose_scheme model.py:417) on that spec for
                                 every BASELINE config, beside the measured
-                                GCells/s of profiles/r01_bench_shared_products.json
+                                GCells/s of profiles/r01_bench.json
 """
 
 from __future__ import annotations
@@ -63,7 +63,7 @@ def star(dims, rad, name):
 
 
 def main():
-    bench = json.load(open(os.path.join(ROOT, "profiles", "r01_bench_shared_products.json")))
+    bench = json.load(open(os.path.join(ROOT, "profiles", "r01_bench.json")))
     cfg = bench.get("configs", {})
     measured = {
         "j2d5pt": (bench["value"], "config 2, 8192^2 x 1000, t=8"),
