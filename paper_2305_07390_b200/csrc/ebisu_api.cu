@@ -382,6 +382,16 @@ std::vector<int> guided_segments(int z_lo, int z_hi, long long tiles, long long 
   return seg_start;
 }
 
+// Dataflow epochs (per-unit completion flags instead of grid.sync between
+// epochs); EBISU_DATAFLOW=0 restores the grid-wide barrier (A/B measurement).
+bool dataflow_epochs() {
+  static const bool on = [] {
+    const char* v = getenv("EBISU_DATAFLOW");
+    return !(v && v[0] == '0');
+  }();
+  return on;
+}
+
 // Per-epoch dynamic-scheduling counters for one stage (zeroed on `st`).
 int alloc_work(int epochs, cudaStream_t st, int** out) {
   EB_CUDA(cudaMallocAsync((void**)out, sizeof(int) * (size_t)std::max(epochs, 1), st));
@@ -447,10 +457,16 @@ int run_tb2d_stage(const ProblemDesc& p, const TbKernel* k, int epochs, int firs
   }
   int* work = nullptr;
   if (int rc = alloc_work(epochs, st, &work)) return rc;
+  int* flags = nullptr;
+  if (coop && dataflow_epochs()) {
+    EB_CUDA(cudaMallocAsync((void**)&flags, sizeof(int) * (size_t)units, st));
+    EB_CUDA(cudaMemsetAsync(flags, 0, sizeof(int) * (size_t)units, st));
+  }
   if (coop) {
     L.epochs = epochs;
     L.cooperative = true;
     L.work = work;
+    L.flags = flags;
     EB_CUDA(k->launch(L));
     ctr->launches += 1;
     ctr->syncs_device += (uint64_t)(epochs - 1);
@@ -469,6 +485,7 @@ int run_tb2d_stage(const ProblemDesc& p, const TbKernel* k, int epochs, int firs
     }
   }
   cudaFreeAsync(work, st);
+  if (flags) cudaFreeAsync(flags, st);
   if (clk) {
     std::vector<long long> h(2 * units);
     EB_CUDA(cudaMemcpyAsync(h.data(), clk, sizeof(long long) * 2 * units,

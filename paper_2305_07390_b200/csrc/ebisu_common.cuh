@@ -76,6 +76,20 @@ __device__ __forceinline__ double ld_shared_if(const double* p, bool pred, doubl
   return r;
 }
 
+// ---- epoch dataflow flags (gpu scope) --------------------------------------
+__device__ __forceinline__ int ld_acquire_gpu(const int* p) {
+  int v;
+  asm volatile("ld.acquire.gpu.global.b32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ void st_release_gpu(int* p, int v) {
+  asm volatile("st.release.gpu.global.b32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+// spin until *p >= v (the producer's release pairs with this acquire)
+__device__ __forceinline__ void wait_flag_geq(const int* p, int v) {
+  while (ld_acquire_gpu(p) < v) __nanosleep(64);
+}
+
 // ---- proxy fences ---------------------------------------------------------
 // Generic-proxy accesses -> later async-proxy (TMA) accesses.
 __device__ __forceinline__ void fence_proxy_async_shared() {

@@ -60,6 +60,7 @@ struct TbLaunch {
   cudaStream_t stream;
   long long* unit_clock;  // optional per-unit timing (profiling)
   int* work;              // per-epoch dynamic-scheduling counters (device)
+  int* flags;             // per-unit completed-epoch flags (dataflow epochs) or null
 };
 
 struct TbKernel {

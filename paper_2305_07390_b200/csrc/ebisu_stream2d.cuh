@@ -63,6 +63,14 @@ struct Stream2DArgs {
   void* buf[3];      // device pointers by BufId (element type E of the kernel)
   long long* unit_clock;  // optional profiling: [units][2] start/end globaltimer (ns)
   int* work;         // per-epoch unit counters (dynamic scheduling), zeroed by the host
+  // Dataflow epochs (non-null, cooperative launch): flags[u] = epochs unit u
+  // has completed.  A unit of epoch e waits only for the epoch-(e-1) units
+  // whose outputs it reads (its strip +-2, the segments within T*R rows) --
+  // the same units that read what it overwrites, so RAW and WAR are both
+  // covered -- instead of a grid-wide barrier: warps that finish an epoch
+  // early start the next one (no epoch tail).  Deadlock-free: units are
+  // claimed epoch by epoch, so every dependency is held by a resident warp.
+  int* flags;
 };
 
 template <class SH, int T, int C, int NW, int S, class E = double>
@@ -395,6 +403,27 @@ __global__ void __launch_bounds__(NW * 32, MINB)
           stream2d_strip(strip, a.nstrips, a.aligned, n1, Cfg::LC, Cfg::VW, Cfg::HX);
       const int r0 = a.seg_start[seg];
       const int r1 = a.seg_start[seg + 1];
+      if (a.flags && e > 0) {
+        // wait for the previous epoch's units that wrote our input region
+        // (rows [r0-TR, r1+TR), columns [X0, X0+LC)); lanes split the checks
+        int lo_seg = seg, hi_seg = seg;
+        while (lo_seg > 0 && a.seg_start[lo_seg] > r0 - TR) --lo_seg;
+        while (hi_seg + 1 < a.nseg && a.seg_start[hi_seg + 1] < r1 + TR) ++hi_seg;
+        const int nseg_dep = hi_seg - lo_seg + 1;
+        for (int d = lane; d < 5 * nseg_dep; d += 32) {
+          const int js = strip - 2 + d % 5;
+          if (js < 0 || js >= a.nstrips) continue;
+          const StripGeom gj =
+              stream2d_strip(js, a.nstrips, a.aligned, n1, Cfg::LC, Cfg::VW, Cfg::HX);
+          // RAW: js wrote what we read; WAR: js reads what we overwrite
+          const bool raw = gj.vlo < g.X0 + Cfg::LC && gj.vhi > g.X0;
+          const bool war = gj.X0 < g.vhi && gj.X0 + Cfg::LC > g.vlo;
+          if (!raw && !war) continue;
+          wait_flag_geq(a.flags + (lo_seg + d / 5) * a.nstrips + js, e);
+        }
+        __syncwarp();
+        fence_proxy_async_global();  // the TMA loads below see those stores
+      }
       const int ka = max(0, r0 - TR);
       const int kb = min(n0, r1 + TR);
       long long t_start = 0;
@@ -422,6 +451,13 @@ __global__ void __launch_bounds__(NW * 32, MINB)
           break;
       }
       ring_cnt += (uint32_t)(kb - ka);
+      if (a.flags) {
+        // publish: every lane's stores, then the flag (release)
+        fence_proxy_async_global();
+        __threadfence();
+        __syncwarp();
+        if (lane == 0) st_release_gpu(a.flags + u, e + 1);
+      }
       if (a.unit_clock && e == 0 && lane == 0) {
         long long t_end;
         asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_end));
@@ -430,7 +466,7 @@ __global__ void __launch_bounds__(NW * 32, MINB)
       }
     }
 
-    if (e + 1 < a.epochs) {
+    if (e + 1 < a.epochs && !a.flags) {
       // Make this epoch's generic-proxy stores visible to the next epoch's
       // TMA (async-proxy) loads issued by other CTAs.
       fence_proxy_async_global();

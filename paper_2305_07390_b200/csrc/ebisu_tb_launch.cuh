@@ -37,6 +37,7 @@ cudaError_t launch_stream2d(const TbLaunch& L) {
   for (int i = 0; i < 3; ++i) a.buf[i] = L.buf[i];
   a.unit_clock = L.unit_clock;
   a.work = L.work;
+  a.flags = L.flags;
   Coefs<SH::NT, E> cf;
   for (int i = 0; i < SH::NT; ++i) cf.c[i] = (E)L.coeffs[i];
   if (L.cooperative) {
