@@ -646,10 +646,15 @@ int run_tb3d_stage(const ProblemDesc& p, const TbKernel* k, int epochs, int firs
   const int span = p.z_hi - p.z_lo;  // output planes of this call
   int nseg = 1, seg_len = span;
   plan_segments(span, tiles, max_ctas, 3 * T * R, std::max(8, 2 * T * R), &nseg, &seg_len);
-  // (never below 4x the per-unit warm-up, which short segments pay in full)
-  const std::vector<int> seg_start = guided_segments(
-      p.z_lo, p.z_hi, tiles, max_ctas, seg_len,
-      std::max(std::max(8, 2 * T * R), 4 * (T * R + T * k->z)), seg_rows_req);
+  // (never below 4x the per-unit warm-up, which short segments pay in full;
+  // EBISU_SEG3D=uniform: the balanced uniform length, for A/B measurement)
+  const char* seg_mode = getenv("EBISU_SEG3D");
+  const bool uniform = seg_mode && strcmp(seg_mode, "uniform") == 0;
+  const int min_len = std::max(std::max(8, 2 * T * R), 4 * (T * R + T * k->z));
+  const std::vector<int> seg_start =
+      guided_segments(p.z_lo, p.z_hi, tiles, max_ctas, seg_len,
+                      uniform ? std::max(seg_len, min_len) : min_len,
+                      (uniform && seg_rows_req <= 0) ? std::max(seg_len, min_len) : seg_rows_req);
   nseg = (int)seg_start.size() - 1;
   const long long units = tiles * nseg;
   int grid = (int)std::min<long long>(max_ctas, units);
