@@ -256,6 +256,17 @@ def extra_configs(eb, device, _native, torch, stream, hbm_peak):
     del d3f, o3f, s3f
     torch.cuda.empty_cache()
 
+    # ---- config 5 geometry on one GPU: j3d7pt 1024^3 (the per-rank slab of
+    # the weak-scaling runs), 100 steps -------------------------------------
+    ext5 = (1024, 1024, 1024)
+    d5 = device.random_grid_device(ext5, seed=1)
+    o5 = torch.empty_like(d5)
+    s5 = torch.empty_like(d5)
+    tr = _timed_sweep(device, torch, d5, st3, 100, o5, s5)
+    rec("config5_j3d7pt_1024_1gpu", st3, ext5, 100, tr)
+    del d5, o5, s5
+    torch.cuda.empty_cache()
+
     # ---- config 3: large halos at 8192^2, overlapped vs halo exchange -------
     ext2 = (8192, 8192)
     d2 = device.random_grid_device(ext2, seed=1)

@@ -444,3 +444,25 @@ def test_fp32_full_size_against_fp64_gpu():
     assert out.dtype == torch.float32 and tr["kernel"] == "stream2d_tb"
     err = (out.double() - ref).abs().max().item()
     assert err <= FP32_RTOL * ref.abs().max().item(), err
+
+
+def test_config5_geometry_1024_cubed_tb_equals_naive():
+    """BASELINE config 5 geometry on one GPU (j3d7pt 1024^3, 8 GiB per array,
+    64-bit offsets): the temporal-blocking sweep equals the one-launch-per-step
+    naive kernel bitwise (both exact), and composes (run(2t) = run(t)∘run(t))."""
+    from paper_2305_07390_b200 import device
+
+    torch = _torch()
+    st = eb.make_benchmark("j3d7pt")
+    d_in = device.random_grid_device((1024, 1024, 1024), seed=9)
+    a = device.sweep_device(d_in, st, 8, t=4)
+    b = device.sweep_device(d_in, st, 8, scheme=_native.SCHEME_NAIVE)
+    cmp = device.compare_device(a, b)
+    assert cmp["mismatches"] == 0, cmp
+    del b
+    half = device.sweep_device(d_in, st, 4, t=4)
+    del d_in
+    c = device.sweep_device(half, st, 4, t=4)
+    cmp = device.compare_device(a, c)
+    assert cmp["mismatches"] == 0, cmp
+    torch.cuda.empty_cache()
