@@ -343,7 +343,7 @@ def main():
         runner = edist.SlabSweep(st, (N0 * world, N1), t=args.t, seed=1, exact=True)
         step = lambda: runner.run(args.tsteps)  # noqa: E731
         cells_per_step = runner.global_interior_cells() * args.tsteps
-        launches_per_step = -(-args.tsteps // args.t)  # one epoch launch per exchange
+        launches_per_step = None  # counted by the runner over the timed region
     else:
         d_in = device.random_grid_device((N0, N1), seed=1)
         d_out = torch.empty_like(d_in)
@@ -361,6 +361,7 @@ def main():
     for _ in range(args.warmup):
         step()
     torch.cuda.synchronize()
+    launches0 = runner.kernel_launches if world > 1 else 0
     if dist:
         dist.barrier()
     sampler = ClockSampler(local)
@@ -420,7 +421,8 @@ def main():
                      "peak_source": f"{peak_kind} hbm_gbs (MEASURED_PEAKS.json)",
                      "algorithmic_bytes": "16 B per interior cell-step (naive load+store)"},
         "clocks": clocks,
-        "gpu_launches": (launches_per_step * args.steps) if launches_per_step else None,
+        "gpu_launches": (launches_per_step * args.steps) if launches_per_step
+        else (runner.kernel_launches - launches0 if world > 1 else None),
     }
     if world == 1:
         line["kernel"] = kernel

@@ -134,6 +134,10 @@ class SlabSweep:
         self.scratch = torch.empty_like(a)
         self.comm = torch.cuda.Stream(self.device) if a.is_cuda else None
         self.overlapped_epochs = 0
+        # kernels launched by the default step (bench gpu_launches claim): a
+        # ranged single-epoch call = frame copy + TB kernel; a full epoch call
+        # = two frame copies (out and scratch) + TB kernel
+        self.kernel_launches = 0
 
     # -- data --------------------------------------------------------------
     def _fill_random(self, a, seed: int):
@@ -226,6 +230,7 @@ class SlabSweep:
         for band in (lo, hi):
             if band:
                 self.step(self.a, self.b, None, t, t, planes=band)
+                self.kernel_launches += 2
         if self.comm is not None:
             torch = self.torch
             compute = torch.cuda.current_stream(self.device)
@@ -234,11 +239,13 @@ class SlabSweep:
                 self._exchange_bands(self.b, lo, hi)
             if inner[1] > inner[0]:
                 self.step(self.a, self.b, None, t, t, planes=inner)
+                self.kernel_launches += 2
             compute.wait_stream(self.comm)  # ghosts of the next epoch landed
         else:
             self._exchange_bands(self.b, lo, hi)
             if inner[1] > inner[0]:
                 self.step(self.a, self.b, None, t, t, planes=inner)
+                self.kernel_launches += 2
         self.overlapped_epochs += 1
 
     # -- sweep ------------------------------------------------------------------
@@ -258,6 +265,7 @@ class SlabSweep:
                 self._epoch_overlapped()
             else:
                 self.step(self.a, self.b, self.scratch, d, d)
+                self.kernel_launches += 3
                 self.a, self.b = self.b, self.a
                 if done + d < steps:
                     self.exchange(self.halo)
