@@ -152,7 +152,7 @@ __host__ __device__ constexpr int pmod(int a) {
 
 // One work unit (warp strip x row segment) of one epoch.  FC selects the
 // frame-column handling (see StripGeom); frame rows are handled per block.
-template <class SH, int T, int C, int S, bool EXACT, bool UNI, int FC, class E>
+template <class SH, int T, int C, int S, bool EXACT, bool UNI, int FC, class E, bool SHIFT = false>
 __device__ __forceinline__ void stream2d_unit(const CUtensorMap* tm, E* __restrict__ out,
                                               E* ring, uint64_t* bars, uint32_t ring_cnt,
                                               int lane, int n0, int n1, const StripGeom& g,
@@ -206,12 +206,35 @@ __device__ __forceinline__ void stream2d_unit(const CUtensorMap* tm, E* __restri
 #pragma unroll
       for (int c = 0; c < C; ++c) win[s][w][c] = 0.0;
 
-  // One unrolled block of W advances.  FROWS: some target row in this block
+  // One unrolled block of UW advances.  FROWS: some target row in this block
   // may be a frame row (only near the top/bottom of the grid).
+  //   rotating windows (default): UW = W advances per block, row q+dy of
+  //     level s-1 sits in slot (k - s*R + dy) mod W, a compile-time register;
+  //   SHIFT (large radii): UW = 1, the window shifts down one slot per
+  //     advance (W*C register moves) and row q+dy sits in slot R+dy -- the
+  //     code is W times smaller, which for W = 13 keeps the loop in the
+  //     instruction cache (the rotating version measured 11.6 % no-instruction
+  //     stalls at R = 6).
+  constexpr int UW = SHIFT ? 1 : W;
+  auto slot_of = [](int uu, int s, int dy) { return SHIFT ? R + dy : pmod<W>(uu - s * R + dy); };
+  auto put = [&](auto lvl_tag, int uu, const E (&v)[C]) {
+    constexpr int L = decltype(lvl_tag)::value;
+    if constexpr (SHIFT) {
+#pragma unroll
+      for (int w = 0; w + 1 < W; ++w)
+#pragma unroll
+        for (int c = 0; c < C; ++c) win[L][w][c] = win[L][w + 1][c];
+#pragma unroll
+      for (int c = 0; c < C; ++c) win[L][W - 1][c] = v[c];
+    } else {
+#pragma unroll
+      for (int c = 0; c < C; ++c) win[L][pmod<W>(uu - L * R)][c] = v[c];
+    }
+  };
   auto block = [&](int kbase, auto frows_tag) {
     constexpr bool FROWS = decltype(frows_tag)::value;
 #pragma unroll
-    for (int uu = 0; uu < W; ++uu) {
+    for (int uu = 0; uu < UW; ++uu) {
       const int k = kbase + uu;
       // ---- level 0: next input row from the TMA ring ----------------------
       // (the select keeps the window write unconditional, so the dead oldest
@@ -248,7 +271,8 @@ __device__ __forceinline__ void stream2d_unit(const CUtensorMap* tm, E* __restri
         }
         // UNI: the window holds products y = c*x (one DMUL per cell per level)
 #pragma unroll
-        for (int c = 0; c < C; ++c) win[0][uu][c] = UNI ? mul_rn<E>(cf.c[0], v[c]) : v[c];
+        for (int c = 0; c < C; ++c) v[c] = UNI ? mul_rn<E>(cf.c[0], v[c]) : v[c];
+        put(std::integral_constant<int, 0>{}, uu, v);
       }
       // ---- levels 1..T ----------------------------------------------------
       // Every level runs every advance.  During pipeline warm-up a level's
@@ -272,7 +296,7 @@ __device__ __forceinline__ void stream2d_unit(const CUtensorMap* tm, E* __restri
               constexpr int ccr = C + j;
               constexpr int dr = ccr / C;
               constexpr int colr = ccr - dr * C;
-              const int sl = pmod<W>(uu - s * R + dy);
+              const int sl = slot_of(uu, s, dy);
               hl[wI][j] = __shfl_up_sync(kFullMask, win[s - 1][sl][coll], dl);
               hr[wI][j] = __shfl_down_sync(kFullMask, win[s - 1][sl][colr], dr);
             });
@@ -285,7 +309,7 @@ __device__ __forceinline__ void stream2d_unit(const CUtensorMap* tm, E* __restri
           constexpr Off o = SH::tap(i);
 #pragma unroll
           for (int c = 0; c < C; ++c) {
-            const int sl = pmod<W>(uu - s * R + o.d0);
+            const int sl = slot_of(uu, s, o.d0);
             const int cc = c + o.d1;
             E x;
             if (cc < 0)
@@ -311,7 +335,7 @@ __device__ __forceinline__ void stream2d_unit(const CUtensorMap* tm, E* __restri
         if constexpr (FROWS) frow = (q < R) || (q >= n0 - R);
 #pragma unroll
         for (int c = 0; c < C; ++c) {
-          const E centre = win[s - 1][pmod<W>(uu - s * R)][c];
+          const E centre = win[s - 1][slot_of(uu, s, 0)][c];
           const E val = (UNI && s < T) ? mul_rn<E>(cf.c[0], acc[c]) : acc[c];
           if (FROWS && col_may_frame(c))
             nv[c] = (frow || fcol[c]) ? centre : val;
@@ -323,8 +347,7 @@ __device__ __forceinline__ void stream2d_unit(const CUtensorMap* tm, E* __restri
             nv[c] = val;
         }
         if constexpr (s < T) {
-#pragma unroll
-          for (int c = 0; c < C; ++c) win[s][pmod<W>(uu - s * R)][c] = nv[c];
+          put(std::integral_constant<int, s>{}, uu, nv);
         } else {
           if (q >= r0 && q < r1) {
             E* orow = out + (size_t)q * (size_t)n1 + (X0 + lane * C);
@@ -343,9 +366,9 @@ __device__ __forceinline__ void stream2d_unit(const CUtensorMap* tm, E* __restri
     }
   };
 
-  for (int kbase = ka; kbase < kend; kbase += W) {
-    // target rows of this block: [kbase - TR, kbase + W - 1 - R]
-    const bool frows = (kbase - TR < R) || (kbase + W - 1 >= n0);
+  for (int kbase = ka; kbase < kend; kbase += UW) {
+    // target rows of this block: [kbase - TR, kbase + UW - 1 - R]
+    const bool frows = (kbase - TR < R) || (kbase + UW - 1 >= n0);
     if (frows)
       block(kbase, std::true_type{});
     else
@@ -360,7 +383,8 @@ __device__ __forceinline__ int next_unit(int* counter, int lane) {
   return __shfl_sync(kFullMask, u, 0);
 }
 
-template <class SH, int T, int C, int NW, int S, bool EXACT, bool UNI, int MINB, class E = double>
+template <class SH, int T, int C, int NW, int S, bool EXACT, bool UNI, int MINB, class E = double,
+          bool SHIFT = false>
 __global__ void __launch_bounds__(NW * 32, MINB)
     k_stream2d(const __grid_constant__ TmapSet maps, const Stream2DArgs a,
                const __grid_constant__ Coefs<SH::NT, E> cf) {
@@ -430,23 +454,23 @@ __global__ void __launch_bounds__(NW * 32, MINB)
       if (a.unit_clock && e == 0 && lane == 0)
         asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_start));
       if constexpr (R > C) {
-        stream2d_unit<SH, T, C, S, EXACT, UNI, 3, E>(tm, out, ring, bars, ring_cnt, lane, n0, n1, g, r0,
+        stream2d_unit<SH, T, C, S, EXACT, UNI, 3, E, SHIFT>(tm, out, ring, bars, ring_cnt, lane, n0, n1, g, r0,
                                              r1, cf);
       } else switch (g.fc) {
         case 0:
-          stream2d_unit<SH, T, C, S, EXACT, UNI, 0, E>(tm, out, ring, bars, ring_cnt, lane, n0, n1, g,
+          stream2d_unit<SH, T, C, S, EXACT, UNI, 0, E, SHIFT>(tm, out, ring, bars, ring_cnt, lane, n0, n1, g,
                                                r0, r1, cf);
           break;
         case 1:
-          stream2d_unit<SH, T, C, S, EXACT, UNI, 1, E>(tm, out, ring, bars, ring_cnt, lane, n0, n1, g,
+          stream2d_unit<SH, T, C, S, EXACT, UNI, 1, E, SHIFT>(tm, out, ring, bars, ring_cnt, lane, n0, n1, g,
                                                r0, r1, cf);
           break;
         case 2:
-          stream2d_unit<SH, T, C, S, EXACT, UNI, 2, E>(tm, out, ring, bars, ring_cnt, lane, n0, n1, g,
+          stream2d_unit<SH, T, C, S, EXACT, UNI, 2, E, SHIFT>(tm, out, ring, bars, ring_cnt, lane, n0, n1, g,
                                                r0, r1, cf);
           break;
         default:
-          stream2d_unit<SH, T, C, S, EXACT, UNI, 3, E>(tm, out, ring, bars, ring_cnt, lane, n0, n1, g,
+          stream2d_unit<SH, T, C, S, EXACT, UNI, 3, E, SHIFT>(tm, out, ring, bars, ring_cnt, lane, n0, n1, g,
                                                r0, r1, cf);
           break;
       }

@@ -11,10 +11,11 @@
 
 namespace ebisu {
 
-template <class SH, int T, int C, int NW, int S, bool EXACT, bool UNI, int MINB, class E>
+template <class SH, int T, int C, int NW, int S, bool EXACT, bool UNI, int MINB, class E,
+          bool SHIFT = false>
 cudaError_t launch_stream2d(const TbLaunch& L) {
   using Cfg = Stream2DCfg<SH, T, C, NW, S, E>;
-  auto kern = k_stream2d<SH, T, C, NW, S, EXACT, UNI, MINB, E>;
+  auto kern = k_stream2d<SH, T, C, NW, S, EXACT, UNI, MINB, E, SHIFT>;
   cudaError_t err =
       cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg::SMEM_BYTES);
   if (err != cudaSuccess) return err;
@@ -61,14 +62,17 @@ constexpr int s2d_minb(int T, int R, int C, int NW, int ebytes = 8) {
   return m < 1 ? 1 : (m > 8 ? 8 : m);
 }
 
-#define EBISU_S2D_ENTRY(SHAPE_ID, SH, T, C, NW, S, EX, UNI, E)                                 \
+#define EBISU_S2D_ENTRY(SHAPE_ID, SH, T, C, NW, S, EX, UNI, E) \
+  EBISU_S2D_ENTRY_SH(SHAPE_ID, SH, T, C, NW, S, EX, UNI, E, false)
+// SHIFT: shifted (not rotating) register windows, see stream2d_unit
+#define EBISU_S2D_ENTRY_SH(SHAPE_ID, SH, T, C, NW, S, EX, UNI, E, SHIFT)                       \
   TbKernel {                                                                                  \
     SHAPE_ID, 2, T, C, NW, S, EX, UNI, Stream2DCfg<SH, T, C, NW, S, E>::SMEM_BYTES, 32 * C, 1, \
         1, Stream2DCfg<SH, T, C, NW, S, E>::VW, 0, 0, 0,                                     \
         (const void*)&k_stream2d<SH, T, C, NW, S, (EX) != 0, (UNI) != 0,                      \
-                                 s2d_minb(T, SH::R, C, NW, (int)sizeof(E)), E>,               \
+                                 s2d_minb(T, SH::R, C, NW, (int)sizeof(E)), E, SHIFT>,        \
         &launch_stream2d<SH, T, C, NW, S, (EX) != 0, (UNI) != 0,                              \
-                         s2d_minb(T, SH::R, C, NW, (int)sizeof(E)), E>,                       \
+                         s2d_minb(T, SH::R, C, NW, (int)sizeof(E)), E, SHIFT>,                \
         0, (int)sizeof(E)                                                                     \
   }
 

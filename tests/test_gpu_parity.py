@@ -466,3 +466,18 @@ def test_config5_geometry_1024_cubed_tb_equals_naive():
     cmp = device.compare_device(a, c)
     assert cmp["mismatches"] == 0, cmp
     torch.cuda.empty_cache()
+
+
+@pytest.mark.parametrize("name", list(CASES_2D))
+def test_2d_every_registered_variant_bitwise(name):
+    """Every registered 2-D kernel variant (e.g. the shifted-window kernels of
+    the large-radius stars) on ragged grids, bitwise against the oracle."""
+    st = _shape(name)
+    for t in CASES_2D[name]:
+        steps = 2 * t + 1
+        for ext in ((2 * st.radius + 41, 262), (129, 2 * (2 * st.radius + 70))):
+            ref = None
+            for g, v, tr, out in _variants(st, t, ext, steps):
+                if ref is None:
+                    ref = oracle_run(g.cells, taps_of(st), steps)
+                assert np.array_equal(out.cells, ref), (name, t, v, ext, tr)
