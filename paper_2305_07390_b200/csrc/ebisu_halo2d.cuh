@@ -84,7 +84,7 @@ struct Halo2DArgs {
 };
 
 // One unit: CTA strip x row segment.  EDGE: the strip touches a frame column.
-template <class SH, int T, int C, int NW, int S, bool EXACT, bool UNI, bool EDGE>
+template <class SH, int T, int C, int NW, int S, bool EXACT, bool UNI, bool EDGE, bool SHIFT>
 __device__ __forceinline__ int halo2d_unit(const CUtensorMap* tm, double* __restrict__ out,
                                            double* ring, uint64_t* bars, double* xh,
                                            uint64_t* advbar, uint32_t ring_cnt, uint32_t& adv,
@@ -96,7 +96,9 @@ __device__ __forceinline__ int halo2d_unit(const CUtensorMap* tm, double* __rest
   constexpr int TZ = T * Z;
 
   const int ka = max(0, r0 - T * R);
-  const int nadv = (r1 + TZ - ka + W - 1) / W * W;  // whole unrolled blocks
+  // SHIFT: shifted windows, one advance per block (see stream2d_unit)
+  constexpr int UW = SHIFT ? 1 : W;
+  const int nadv = (r1 + TZ - ka + UW - 1) / UW * UW;  // whole unrolled blocks
   const int kend = ka + nadv;
   const int XW = X0 + warp * LC;  // this warp's first column
 
@@ -151,7 +153,7 @@ __device__ __forceinline__ int halo2d_unit(const CUtensorMap* tm, double* __rest
   auto block = [&](int kbase, auto frows_tag) {
     constexpr bool FROWS = decltype(frows_tag)::value;
 #pragma unroll
-    for (int uu = 0; uu < W; ++uu) {
+    for (int uu = 0; uu < UW; ++uu) {
       const int k = kbase + uu;
       const int bk = k & (NB - 1);
       // (DR barriers round robin: advance a arrives on advbar[a % DR] as its
@@ -179,7 +181,15 @@ __device__ __forceinline__ int halo2d_unit(const CUtensorMap* tm, double* __rest
           v[c + 1] = UNI ? __dmul_rn(cf.c[0], t2.y) : t2.y;
         }
 #pragma unroll
-        for (int c = 0; c < C; ++c) win[0][uu][c] = v[c];
+        for (int c = 0; c < C; ++c) {
+          if constexpr (SHIFT) {
+#pragma unroll
+            for (int w = 0; w + 1 < W; ++w) win[0][w][c] = win[0][w + 1][c];
+            win[0][W - 1][c] = v[c];
+          } else {
+            win[0][uu][c] = v[c];
+          }
+        }
         push(0, bk, v);
       }
       // ---- levels 1..T --------------------------------------------------------
@@ -190,7 +200,7 @@ __device__ __forceinline__ int halo2d_unit(const CUtensorMap* tm, double* __rest
         static_for<2 * R + 1>([&](auto dI) {
           constexpr int dy = decltype(dI)::value - R;
           if constexpr (row_has_halo<SH>(dy)) {
-            const int sl = pmod<W>(uu - s * Z + dy);
+            const int sl = SHIFT ? R + dy : pmod<W>(uu - s * Z + dy);
             const int xs = (k - Z + dy) & (NB - 1);  // advance that produced the row
             const double* Lb = xrow(s - 1, xs, wr, 0);   // right neighbour's left edge
             const double* Rb = xrow(s - 1, xs, wl, 1);   // left neighbour's right edge
@@ -219,7 +229,7 @@ __device__ __forceinline__ int halo2d_unit(const CUtensorMap* tm, double* __rest
           constexpr Off o = SH::tap(i);
 #pragma unroll
           for (int c = 0; c < C; ++c) {
-            const int sl = pmod<W>(uu - s * Z + o.d0);
+            const int sl = SHIFT ? R + o.d0 : pmod<W>(uu - s * Z + o.d0);
             const int cc = c + o.d1;
             double x;
             if (cc < 0)
@@ -241,7 +251,7 @@ __device__ __forceinline__ int halo2d_unit(const CUtensorMap* tm, double* __rest
         double nv[C];
 #pragma unroll
         for (int c = 0; c < C; ++c) {
-          const double centre = win[s - 1][pmod<W>(uu - s * Z)][c];
+          const double centre = win[s - 1][SHIFT ? R : pmod<W>(uu - s * Z)][c];
           const double val = (UNI && s < T) ? __dmul_rn(cf.c[0], acc[c]) : acc[c];
           if constexpr (EDGE || FROWS) {
             bool f = frow;
@@ -253,7 +263,15 @@ __device__ __forceinline__ int halo2d_unit(const CUtensorMap* tm, double* __rest
         }
         if constexpr (s < T) {
 #pragma unroll
-          for (int c = 0; c < C; ++c) win[s][pmod<W>(uu - s * Z)][c] = nv[c];
+          for (int c = 0; c < C; ++c) {
+            if constexpr (SHIFT) {
+#pragma unroll
+              for (int w = 0; w + 1 < W; ++w) win[s][w][c] = win[s][w + 1][c];
+              win[s][W - 1][c] = nv[c];
+            } else {
+              win[s][pmod<W>(uu - s * Z)][c] = nv[c];
+            }
+          }
           push(s, bk, nv);
         } else {
           bool qok = (q >= r0) && (q < r1);
@@ -272,9 +290,9 @@ __device__ __forceinline__ int halo2d_unit(const CUtensorMap* tm, double* __rest
     }
   };
 
-  for (int kbase = ka; kbase < kend; kbase += W) {
-    // target rows of this block: [kbase - TZ, kbase + W - 1 - Z]
-    if ((kbase - TZ < R) || (kbase + W - 1 - Z >= n0 - R))
+  for (int kbase = ka; kbase < kend; kbase += UW) {
+    // target rows of this block: [kbase - TZ, kbase + UW - 1 - Z]
+    if ((kbase - TZ < R) || (kbase + UW - 1 - Z >= n0 - R))
       block(kbase, std::true_type{});
     else
       block(kbase, std::false_type{});
@@ -282,7 +300,8 @@ __device__ __forceinline__ int halo2d_unit(const CUtensorMap* tm, double* __rest
   return nadv;
 }
 
-template <class SH, int T, int C, int NW, int S, bool EXACT, bool UNI, int MINB>
+template <class SH, int T, int C, int NW, int S, bool EXACT, bool UNI, int MINB,
+          bool SHIFT = false>
 __global__ void __launch_bounds__(NW * 32, MINB)
     k_halo2d(const __grid_constant__ TmapSet maps, const Halo2DArgs a,
              const __grid_constant__ Coefs<SH::NT> cf) {
@@ -330,11 +349,11 @@ __global__ void __launch_bounds__(NW * 32, MINB)
       const bool edge = (g.X0 < Cfg::R) || (g.X0 + Cfg::LW > n1 - Cfg::R);
       int used;
       if (edge)
-        used = halo2d_unit<SH, T, C, NW, S, EXACT, UNI, true>(
+        used = halo2d_unit<SH, T, C, NW, S, EXACT, UNI, true, SHIFT>(
             tm, out, ring, bars, xh, advbar, ring_cnt, adv, warp, lane, n0, n1, g.X0, g.vlo,
             g.vhi, r0, r1, cf);
       else
-        used = halo2d_unit<SH, T, C, NW, S, EXACT, UNI, false>(
+        used = halo2d_unit<SH, T, C, NW, S, EXACT, UNI, false, SHIFT>(
             tm, out, ring, bars, xh, advbar, ring_cnt, adv, warp, lane, n0, n1, g.X0, g.vlo,
             g.vhi, r0, r1, cf);
       ring_cnt += (uint32_t)used;

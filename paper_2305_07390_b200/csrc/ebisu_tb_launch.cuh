@@ -132,10 +132,11 @@ cudaError_t launch_stream3d(const TbLaunch& L) {
         (int)sizeof(E)                                                                        \
   }
 
-template <class SH, int T, int C, int NW, int S, bool EXACT, bool UNI, int MINB>
+template <class SH, int T, int C, int NW, int S, bool EXACT, bool UNI, int MINB,
+          bool SHIFT = false>
 cudaError_t launch_halo2d(const TbLaunch& L) {
   using Cfg = Halo2DCfg<SH, T, C, NW, S>;
-  auto kern = k_halo2d<SH, T, C, NW, S, EXACT, UNI, MINB>;
+  auto kern = k_halo2d<SH, T, C, NW, S, EXACT, UNI, MINB, SHIFT>;
   cudaError_t err =
       cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg::SMEM_BYTES);
   if (err != cudaSuccess) return err;
@@ -168,13 +169,15 @@ cudaError_t launch_halo2d(const TbLaunch& L) {
 
 // box0 = warp columns (TMA box), valid_x = valid columns per CTA strip, C =
 // cells per lane, z = level skew, wn = strip columns (LW)
-#define EBISU_H2D_ENTRY(SHAPE_ID, SH, T, C, NW, S, EX, UNI, MINB)                              \
+#define EBISU_H2D_ENTRY(SHAPE_ID, SH, T, C, NW, S, EX, UNI, MINB) \
+  EBISU_H2D_ENTRY_SH(SHAPE_ID, SH, T, C, NW, S, EX, UNI, MINB, false)
+#define EBISU_H2D_ENTRY_SH(SHAPE_ID, SH, T, C, NW, S, EX, UNI, MINB, SHIFT)                    \
   TbKernel {                                                                                  \
     SHAPE_ID, 2, T, C, NW, S, EX, UNI, Halo2DCfg<SH, T, C, NW, S>::SMEM_BYTES, 32 * C, 1, 1,   \
         Halo2DCfg<SH, T, C, NW, S>::VW, 0, Halo2DCfg<SH, T, C, NW, S>::Z,                     \
         Halo2DCfg<SH, T, C, NW, S>::LW,                                                       \
-        (const void*)&k_halo2d<SH, T, C, NW, S, (EX) != 0, (UNI) != 0, MINB>,                 \
-        &launch_halo2d<SH, T, C, NW, S, (EX) != 0, (UNI) != 0, MINB>, 1, 8                   \
+        (const void*)&k_halo2d<SH, T, C, NW, S, (EX) != 0, (UNI) != 0, MINB, SHIFT>,          \
+        &launch_halo2d<SH, T, C, NW, S, (EX) != 0, (UNI) != 0, MINB, SHIFT>, 1, 8             \
   }
 
 }  // namespace ebisu

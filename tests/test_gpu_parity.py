@@ -128,11 +128,11 @@ def test_3d_shapes_all_depths_ragged(name):
             assert np.array_equal(out.cells, ref), (name, t, (n0, n1, n2), steps, tr)
 
 
-def _variants(st, t, ext, steps):
+def _variants(st, t, ext, steps, scheme=0):
     """Yield (variant, trace, output) for every registered kernel variant."""
     g = eb.random_grid(ext, 97 + t)
     for v in range(64):
-        prm = _native.make_params(t=t, variant=v)
+        prm = _native.make_params(t=t, variant=v, scheme=scheme)
         try:
             out, tr = eb.sweep(g, st, steps, params=prm, trace=True)
         except Exception as e:  # past the last registered variant
@@ -477,7 +477,8 @@ def test_2d_every_registered_variant_bitwise(name):
         steps = 2 * t + 1
         for ext in ((2 * st.radius + 41, 262), (129, 2 * (2 * st.radius + 70))):
             ref = None
-            for g, v, tr, out in _variants(st, t, ext, steps):
-                if ref is None:
-                    ref = oracle_run(g.cells, taps_of(st), steps)
-                assert np.array_equal(out.cells, ref), (name, t, v, ext, tr)
+            for scheme in (_native.SCHEME_SM_TILING, _native.SCHEME_DEVICE_TILING):
+                for g, v, tr, out in _variants(st, t, ext, steps, scheme):
+                    if ref is None:
+                        ref = oracle_run(g.cells, taps_of(st), steps)
+                    assert np.array_equal(out.cells, ref), (name, t, v, scheme, ext, tr)
