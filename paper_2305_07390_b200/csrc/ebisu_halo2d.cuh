@@ -61,9 +61,7 @@ struct Halo2DCfg {
   static constexpr int ROW_BYTES = LC * 8;
   static constexpr int RING_BYTES = NW * S * ROW_BYTES;
   static constexpr int XH_DOUBLES = T * NB * NW * 2 * R;  // levels 0..T-1
-  static constexpr int JUNK_DOUBLES = 0;
-  static constexpr int SMEM_BYTES =
-      RING_BYTES + (XH_DOUBLES + JUNK_DOUBLES) * 8 + (NW * S + DR) * 8;
+  static constexpr int SMEM_BYTES = RING_BYTES + XH_DOUBLES * 8 + (NW * S + DR) * 8;
   static_assert(VW > 0, "strip leaves no valid core");
   static_assert(NB >= NBMIN, "edge-buffer slots must cover lag + drift");
   static_assert((S & (S - 1)) == 0, "ring slots must be a power of two");
@@ -310,8 +308,7 @@ __global__ void __launch_bounds__(NW * 32, MINB)
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   double* ring = reinterpret_cast<double*>(smem + warp * S * Cfg::ROW_BYTES);
   double* xh = reinterpret_cast<double*>(smem + Cfg::RING_BYTES);
-  uint64_t* bars_all = reinterpret_cast<uint64_t*>(
-      smem + Cfg::RING_BYTES + (Cfg::XH_DOUBLES + Cfg::JUNK_DOUBLES) * 8);
+  uint64_t* bars_all = reinterpret_cast<uint64_t*>(smem + Cfg::RING_BYTES + Cfg::XH_DOUBLES * 8);
   uint64_t* bars = bars_all + warp * S;
   uint64_t* advbar = bars_all + NW * S;
 
