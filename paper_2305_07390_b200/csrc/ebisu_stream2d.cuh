@@ -152,7 +152,7 @@ __host__ __device__ constexpr int pmod(int a) {
 
 // One work unit (warp strip x row segment) of one epoch.  FC selects the
 // frame-column handling (see StripGeom); frame rows are handled per block.
-template <class SH, int T, int C, int S, bool EXACT, bool UNI, int FC, class E, bool SHIFT = false>
+template <class SH, int T, int C, int S, bool EXACT, bool UNI, int FC, class E, int SHIFT = 0>
 __device__ __forceinline__ void stream2d_unit(const CUtensorMap* tm, E* __restrict__ out,
                                               E* ring, uint64_t* bars, uint32_t ring_cnt,
                                               int lane, int n0, int n1, const StripGeom& g,
@@ -198,34 +198,37 @@ __device__ __forceinline__ void stream2d_unit(const CUtensorMap* tm, E* __restri
     return FC == 3 || (FC == 1 && c < R) || (FC == 2 && c >= C - R);
   };
 
-  E win[T][W][C];
+  // SHIFT = U > 0: W + U - 1 slots per level (the W - 1 carried rows and the
+  // U rows produced by one unrolled block)
+  constexpr int WS = SHIFT ? W + SHIFT - 1 : W;
+  E win[T][WS][C];
 #pragma unroll
   for (int s = 0; s < T; ++s)
 #pragma unroll
-    for (int w = 0; w < W; ++w)
+    for (int w = 0; w < WS; ++w)
 #pragma unroll
       for (int c = 0; c < C; ++c) win[s][w][c] = 0.0;
 
   // One unrolled block of UW advances.  FROWS: some target row in this block
   // may be a frame row (only near the top/bottom of the grid).
-  //   rotating windows (default): UW = W advances per block, row q+dy of
+  //   rotating windows (SHIFT = 0): UW = W advances per block, row q+dy of
   //     level s-1 sits in slot (k - s*R + dy) mod W, a compile-time register;
-  //   SHIFT (large radii): UW = 1, the window shifts down one slot per
-  //     advance (W*C register moves) and row q+dy sits in slot R+dy -- the
-  //     code is W times smaller, which for W = 13 keeps the loop in the
-  //     instruction cache (the rotating version measured 11.6 % no-instruction
-  //     stalls at R = 6).
-  constexpr int UW = SHIFT ? 1 : W;
-  auto slot_of = [](int uu, int s, int dy) { return SHIFT ? R + dy : pmod<W>(uu - s * R + dy); };
+  //   shifted windows (SHIFT = U, large radii): UW = U advances per block;
+  //     inner advance uu writes its row to slot W-1+uu and reads row q+dy
+  //     from slot R+dy+uu; after the block the window shifts down by U
+  //     ((W-1)*C register moves per U advances).  The code is W/U times
+  //     smaller than the rotating version, which for W = 13 keeps the loop in
+  //     the instruction cache (the rotating kernel measured 11.6 %
+  //     no-instruction stalls at R = 6).
+  constexpr int UW = SHIFT ? SHIFT : W;
+  auto slot_of = [](int uu, int s, int dy) {
+    return SHIFT ? R + dy + uu : pmod<W>(uu - s * R + dy);
+  };
   auto put = [&](auto lvl_tag, int uu, const E (&v)[C]) {
     constexpr int L = decltype(lvl_tag)::value;
     if constexpr (SHIFT) {
 #pragma unroll
-      for (int w = 0; w + 1 < W; ++w)
-#pragma unroll
-        for (int c = 0; c < C; ++c) win[L][w][c] = win[L][w + 1][c];
-#pragma unroll
-      for (int c = 0; c < C; ++c) win[L][W - 1][c] = v[c];
+      for (int c = 0; c < C; ++c) win[L][W - 1 + uu][c] = v[c];
     } else {
 #pragma unroll
       for (int c = 0; c < C; ++c) win[L][pmod<W>(uu - L * R)][c] = v[c];
@@ -364,6 +367,15 @@ __device__ __forceinline__ void stream2d_unit(const CUtensorMap* tm, E* __restri
         }
       });
     }
+    if constexpr (SHIFT) {
+      // keep the W-1 newest rows of every level for the next block
+#pragma unroll
+      for (int L = 0; L < T; ++L)
+#pragma unroll
+        for (int w = 0; w + 1 < W; ++w)
+#pragma unroll
+          for (int c = 0; c < C; ++c) win[L][w][c] = win[L][w + SHIFT][c];
+    }
   };
 
   for (int kbase = ka; kbase < kend; kbase += UW) {
@@ -384,7 +396,7 @@ __device__ __forceinline__ int next_unit(int* counter, int lane) {
 }
 
 template <class SH, int T, int C, int NW, int S, bool EXACT, bool UNI, int MINB, class E = double,
-          bool SHIFT = false>
+          int SHIFT = 0>
 __global__ void __launch_bounds__(NW * 32, MINB)
     k_stream2d(const __grid_constant__ TmapSet maps, const Stream2DArgs a,
                const __grid_constant__ Coefs<SH::NT, E> cf) {

@@ -12,7 +12,7 @@
 namespace ebisu {
 
 template <class SH, int T, int C, int NW, int S, bool EXACT, bool UNI, int MINB, class E,
-          bool SHIFT = false>
+          int SHIFT = 0>
 cudaError_t launch_stream2d(const TbLaunch& L) {
   using Cfg = Stream2DCfg<SH, T, C, NW, S, E>;
   auto kern = k_stream2d<SH, T, C, NW, S, EXACT, UNI, MINB, E, SHIFT>;
@@ -63,8 +63,9 @@ constexpr int s2d_minb(int T, int R, int C, int NW, int ebytes = 8) {
 }
 
 #define EBISU_S2D_ENTRY(SHAPE_ID, SH, T, C, NW, S, EX, UNI, E) \
-  EBISU_S2D_ENTRY_SH(SHAPE_ID, SH, T, C, NW, S, EX, UNI, E, false)
-// SHIFT: shifted (not rotating) register windows, see stream2d_unit
+  EBISU_S2D_ENTRY_SH(SHAPE_ID, SH, T, C, NW, S, EX, UNI, E, 0)
+// SHIFT: 0 = rotating register windows, U > 0 = shifted windows with U
+// advances per unrolled block (see stream2d_unit)
 #define EBISU_S2D_ENTRY_SH(SHAPE_ID, SH, T, C, NW, S, EX, UNI, E, SHIFT)                       \
   TbKernel {                                                                                  \
     SHAPE_ID, 2, T, C, NW, S, EX, UNI, Stream2DCfg<SH, T, C, NW, S, E>::SMEM_BYTES, 32 * C, 1, \
