@@ -18,9 +18,18 @@
  *     taps summed in the order given), within 1e-12 relative otherwise.
  *     The input is never modified (reference purity, test_grid.py:152-157).
  *
+ *   ebisu_run_host_f32 / ebisu_run_device_f32
+ *     the same contract in binary32 (no reference counterpart: Grid forces
+ *     float64, grid.py:38); the north-star fp32 mode, within 1e-5 relative
+ *     of reference_run.
+ *
  *   ebisu_random_grid_device
  *     replaces stencilplan.grid.random_grid / rng.uniform_array
  *              (grid.py:56-60, rng.py:31-46), bit-identical draws.
+ *
+ *   ebisu_compare_device
+ *     replaces the planner's parity check np.array_equal + first mismatch
+ *              (planner.py:227-232) on device-resident grids.
  *
  *   ebisu_check_compatible
  *     replaces grid._check_compatible (grid.py:63-73) and
@@ -28,7 +37,8 @@
  *
  * Conventions: plain C types only; no exceptions cross the ABI; every call
  * returns an ebisu_status and, on failure, leaves a thread-local message for
- * ebisu_last_error().  Grids are dense C-order float64 arrays, axis 0 slowest
+ * ebisu_last_error().  Grids are dense C-order float64 (or, for the _f32
+ * entry points, float32) arrays, axis 0 slowest
  * (the streaming axis).  The caller owns every buffer it passes; the library
  * owns only device scratch it allocates itself (released by
  * ebisu_release_scratch).  Calls are reentrant; one CUDA stream per call.
