@@ -171,34 +171,42 @@ class SlabSweep:
         return n
 
     # -- communication ---------------------------------------------------------
+    def _p2p(self, pairs):
+        """Batched point-to-point exchange of (send, recv, peer) triples.
+        NCCL moves device tensors directly; a backend without device P2P
+        (gloo: the single-GPU multi-rank tests) stages them through host
+        memory."""
+        dist = self.dist
+        staged = []
+        ops = []
+        host = dist.get_backend(self.group) == "gloo"
+        for send, recv, peer in pairs:
+            if host and send.is_cuda:
+                hs, hr = send.cpu(), self.torch.empty(recv.shape, dtype=recv.dtype)
+                staged.append((hr, recv))
+                send, recv = hs, hr
+            ops.append(dist.P2POp(dist.isend, send, peer, self.group))
+            ops.append(dist.P2POp(dist.irecv, recv, peer, self.group))
+        if ops:
+            for w in dist.batch_isend_irecv(ops):
+                w.wait()
+        for hr, recv in staged:
+            recv.copy_(hr)
+
     def exchange(self, depth: int):
         """Refresh ``depth`` ghost planes on each interior face."""
         if self.world == 1 or depth == 0:
             return
-        dist = self.dist
         p = self.plan
         a = self.a
-        own_n = p.own1 - p.own0
-        ops = []
-        recv_lo = recv_hi = None
+        lo0 = p.ghost_lo
+        hi0 = p.ghost_lo + (p.own1 - p.own0)
+        pairs = []
         if p.rank > 0:
-            send_lo = a[p.ghost_lo:p.ghost_lo + depth].contiguous()
-            recv_lo = self.torch.empty_like(send_lo)
-            ops.append(dist.P2POp(dist.isend, send_lo, p.rank - 1, self.group))
-            ops.append(dist.P2POp(dist.irecv, recv_lo, p.rank - 1, self.group))
+            pairs.append((a[lo0:lo0 + depth], a[lo0 - depth:lo0], p.rank - 1))
         if p.rank < p.world - 1:
-            hi0 = p.ghost_lo + own_n
-            send_hi = a[hi0 - depth:hi0].contiguous()
-            recv_hi = self.torch.empty_like(send_hi)
-            ops.append(dist.P2POp(dist.isend, send_hi, p.rank + 1, self.group))
-            ops.append(dist.P2POp(dist.irecv, recv_hi, p.rank + 1, self.group))
-        for w in dist.batch_isend_irecv(ops):
-            w.wait()
-        if recv_lo is not None:
-            a[p.ghost_lo - depth:p.ghost_lo].copy_(recv_lo)
-        if recv_hi is not None:
-            hi0 = p.ghost_lo + own_n
-            a[hi0:hi0 + depth].copy_(recv_hi)
+            pairs.append((a[hi0 - depth:hi0], a[hi0:hi0 + depth], p.rank + 1))
+        self._p2p(pairs)
 
     def _bands(self):
         """Local plane ranges: (lower band, upper band, interior) of the owned
@@ -212,16 +220,13 @@ class SlabSweep:
     def _exchange_bands(self, dst, lo, hi):
         """Send the freshly computed bands of ``dst``; receive the neighbours'
         bands straight into the ghost planes of ``dst``."""
-        dist, p, H = self.dist, self.plan, self.halo
-        ops = []
+        p, H = self.plan, self.halo
+        pairs = []
         if lo:
-            ops.append(dist.P2POp(dist.isend, dst[lo[0]:lo[1]], p.rank - 1, self.group))
-            ops.append(dist.P2POp(dist.irecv, dst[lo[0] - H:lo[0]], p.rank - 1, self.group))
+            pairs.append((dst[lo[0]:lo[1]], dst[lo[0] - H:lo[0]], p.rank - 1))
         if hi:
-            ops.append(dist.P2POp(dist.isend, dst[hi[0]:hi[1]], p.rank + 1, self.group))
-            ops.append(dist.P2POp(dist.irecv, dst[hi[1]:hi[1] + H], p.rank + 1, self.group))
-        for w in dist.batch_isend_irecv(ops):
-            w.wait()
+            pairs.append((dst[hi[0]:hi[1]], dst[hi[1]:hi[1] + H], p.rank + 1))
+        self._p2p(pairs)
 
     def _epoch_overlapped(self):
         """One t-step epoch: bands, then exchange (comm stream) || interior."""
@@ -282,6 +287,8 @@ class SlabSweep:
         if self.world == 1:
             return own.cpu()
         sizes = [slab_plan(self.extents[0], self.world, r, self.halo) for r in range(self.world)]
+        # gloo has no device P2P: stage through host memory (tests)
+        dev = "cpu" if dist.get_backend(self.group) == "gloo" else own.device
         if self.rank == dst:
             parts = []
             for r, pr in enumerate(sizes):
@@ -289,9 +296,9 @@ class SlabSweep:
                     parts.append(own.cpu())
                 else:
                     buf = torch.empty((pr.own1 - pr.own0,) + self.extents[1:],
-                                      dtype=torch.float64, device=own.device)
+                                      dtype=own.dtype, device=dev)
                     dist.recv(buf, src=r, group=self.group)
                     parts.append(buf.cpu())
             return torch.cat(parts, 0)
-        dist.send(own, dst=dst, group=self.group)
+        dist.send(own.to(dev), dst=dst, group=self.group)
         return None
