@@ -58,7 +58,7 @@
 extern "C" {
 #endif
 
-#define EBISU_ABI_VERSION 1
+#define EBISU_ABI_VERSION 2  /* 2: ebisu_params.frame_ready, fp32 entry points */
 #define EBISU_MAX_DIMS 3
 #define EBISU_MAX_TAPS 128
 
@@ -107,6 +107,9 @@ typedef struct ebisu_params {
                                 = all.  Needs a single fused epoch (steps <= t): the
                                 multi-GPU driver computes its boundary band first,
                                 sends it, and computes the interior while NCCL runs */
+  int32_t frame_ready;       /* 1: d_out (and d_scratch) already hold the input's
+                                Dirichlet frame, skip the frame pre-copy (repeated
+                                epochs into the same buffers) */
 } ebisu_params;
 /* Shared products: when every coefficient of the stencil is bitwise equal (the
  * catalog default 1/|taps|, shapes.py:148-157), term_k = RN(c*x_k) depends on

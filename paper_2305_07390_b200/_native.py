@@ -30,6 +30,8 @@ SCHEME_SM_TILING = 2
 SCHEME_DEVICE_TILING = 3
 
 # Every symbol include/ebisu.h declares (checked by tests/test_native_abi.py).
+ABI_VERSION = 2  # include/ebisu.h EBISU_ABI_VERSION (ParamsC layout below)
+
 EXPORTS = (
     "ebisu_abi_version",
     "ebisu_last_error",
@@ -78,6 +80,7 @@ class ParamsC(ctypes.Structure):
         ("variant", ctypes.c_int32),
         ("per_tap_products", ctypes.c_int32),
         ("out_planes", ctypes.c_int32 * 2),
+        ("frame_ready", ctypes.c_int32),
     ]
 
 
@@ -154,7 +157,7 @@ def load() -> ctypes.CDLL:
         lib.ebisu_compare_device.argtypes = [vp, vp, i64, ctypes.POINTER(i64),
                                              ctypes.POINTER(i64), dp, dp, vp]
         lib.ebisu_release_scratch.restype = i32
-        if lib.ebisu_abi_version() != 1:
+        if lib.ebisu_abi_version() != ABI_VERSION:
             raise NativeUnavailable("libebisu ABI version mismatch")
         _lib = lib
         return lib
@@ -199,7 +202,8 @@ def make_params(scheme: int = SCHEME_AUTO, t: int = 0, tile=(0, 0), device_tile_
                 lazy: bool = False, exact: bool = True, persistent: bool = True,
                 validate_tile: bool = False, lane_cells: int = 0,
                 seg_rows: int = 0, variant: int = 0,
-                per_tap_products: bool = False, out_planes=(0, 0)) -> ParamsC:
+                per_tap_products: bool = False, out_planes=(0, 0),
+                frame_ready: bool = False) -> ParamsC:
     p = ParamsC()
     p.scheme = scheme
     p.t = int(t)
@@ -216,6 +220,7 @@ def make_params(scheme: int = SCHEME_AUTO, t: int = 0, tile=(0, 0), device_tile_
     p.variant = int(variant)
     p.per_tap_products = int(bool(per_tap_products))
     p.out_planes[0], p.out_planes[1] = int(out_planes[0]), int(out_planes[1])
+    p.frame_ready = int(bool(frame_ready))
     return p
 
 

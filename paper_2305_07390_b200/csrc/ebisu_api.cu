@@ -818,7 +818,7 @@ int run_device_impl(const ProblemDesc& p0, const void* d_in, void* d_out, void* 
   // ping-pong buffers (a shell of 2R planes/rows/columns, not the grid).
   bool any_uni = false;
   for (auto& s : stages) any_uni = any_uni || (s.k && s.k->uni);
-  if (any_uni) {
+  if (any_uni && !(prm && prm->frame_ready)) {
     for (int b = BUF_OUT; b <= BUF_SCR; ++b) {
       if (!bufs[b]) continue;
       cudaError_t e = launch_frame_copy(p, d_in, bufs[b], st, di.sms);

@@ -78,11 +78,14 @@ def slab_plan(n0: int, world: int, rank: int, halo: int) -> SlabPlan:
 def _default_step(stencil: StencilShape, exact: bool):
     from . import _native, device
 
-    def step(src, dst, scratch, steps, t, planes=None):
+    def step(src, dst, scratch, steps, t, planes=None, frame_ready=False):
         if planes is None:
             device.sweep_device(src, stencil, steps, out=dst, scratch=scratch, t=t, exact=exact)
         else:
-            prm = _native.make_params(t=t, exact=exact, out_planes=planes)
+            # frame_ready: dst already holds the (constant) frame, so the
+            # ranged call skips its frame pre-copy launch
+            prm = _native.make_params(t=t, exact=exact, out_planes=planes,
+                                      frame_ready=frame_ready)
             device.sweep_device(src, stencil, steps, out=dst, params=prm)
 
     return step
@@ -134,6 +137,9 @@ class SlabSweep:
         self.scratch = torch.empty_like(a)
         self.comm = torch.cuda.Stream(self.device) if a.is_cuda else None
         self.overlapped_epochs = 0
+        # buffers holding the Dirichlet frame (the input does; an epoch's
+        # output does once its ranged calls copied theirs)
+        self._framed = {a.data_ptr()}
         # kernels launched by the default step (bench gpu_launches claim): a
         # ranged single-epoch call = frame copy + TB kernel; a full epoch call
         # = two frame copies (out and scratch) + TB kernel
@@ -232,10 +238,12 @@ class SlabSweep:
         """One t-step epoch: bands, then exchange (comm stream) || interior."""
         t = self.t
         lo, hi, inner = self._bands()
+        ready = self.b.data_ptr() in self._framed
+        per_call = 1 if ready else 2  # TB kernel (+ frame pre-copy)
         for band in (lo, hi):
             if band:
-                self.step(self.a, self.b, None, t, t, planes=band)
-                self.kernel_launches += 2
+                self.step(self.a, self.b, None, t, t, planes=band, frame_ready=ready)
+                self.kernel_launches += per_call
         if self.comm is not None:
             torch = self.torch
             compute = torch.cuda.current_stream(self.device)
@@ -243,14 +251,15 @@ class SlabSweep:
             with torch.cuda.stream(self.comm):
                 self._exchange_bands(self.b, lo, hi)
             if inner[1] > inner[0]:
-                self.step(self.a, self.b, None, t, t, planes=inner)
-                self.kernel_launches += 2
+                self.step(self.a, self.b, None, t, t, planes=inner, frame_ready=ready)
+                self.kernel_launches += per_call
             compute.wait_stream(self.comm)  # ghosts of the next epoch landed
         else:
             self._exchange_bands(self.b, lo, hi)
             if inner[1] > inner[0]:
-                self.step(self.a, self.b, None, t, t, planes=inner)
-                self.kernel_launches += 2
+                self.step(self.a, self.b, None, t, t, planes=inner, frame_ready=ready)
+                self.kernel_launches += per_call
+        self._framed.add(self.b.data_ptr())
         self.overlapped_epochs += 1
 
     # -- sweep ------------------------------------------------------------------
@@ -271,6 +280,7 @@ class SlabSweep:
             else:
                 self.step(self.a, self.b, self.scratch, d, d)
                 self.kernel_launches += 3
+                self._framed.update((self.b.data_ptr(), self.scratch.data_ptr()))
                 self.a, self.b = self.b, self.a
                 if done + d < steps:
                     self.exchange(self.halo)

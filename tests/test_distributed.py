@@ -51,7 +51,7 @@ def _worker(rank, world, port, results):
             st = eb.get_shape(name)
             taps = taps_of(st)
 
-            def step(src, dst, scratch, n, _t, planes=None, taps=taps):
+            def step(src, dst, scratch, n, _t, planes=None, frame_ready=False, taps=taps):
                 # same contract as the kernel: ``planes`` restricts the planes
                 # written (ebisu_params.out_planes); the rest of dst is untouched
                 res = torch.from_numpy(reference_run(src.numpy(), taps, n))
