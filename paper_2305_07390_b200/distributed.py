@@ -235,30 +235,40 @@ class SlabSweep:
         self._p2p(pairs)
 
     def _epoch_overlapped(self):
-        """One t-step epoch: bands, then exchange (comm stream) || interior."""
+        """One t-step epoch.  Communication stream: the two boundary bands,
+        then their exchange; compute stream, concurrently: the interior.  The
+        bands are launched first so their few CTAs get SMs before the
+        interior grid fills the rest; band kernel and exchange both leave the
+        critical path (the interior takes longer than either)."""
         t = self.t
         lo, hi, inner = self._bands()
         ready = self.b.data_ptr() in self._framed
         per_call = 1 if ready else 2  # TB kernel (+ frame pre-copy)
-        for band in (lo, hi):
-            if band:
-                self.step(self.a, self.b, None, t, t, planes=band, frame_ready=ready)
+
+        def bands():
+            for band in (lo, hi):
+                if band:
+                    self.step(self.a, self.b, None, t, t, planes=band, frame_ready=ready)
+                    self.kernel_launches += per_call
+
+        def interior():
+            if inner[1] > inner[0]:
+                self.step(self.a, self.b, None, t, t, planes=inner, frame_ready=ready)
                 self.kernel_launches += per_call
+
         if self.comm is not None:
             torch = self.torch
             compute = torch.cuda.current_stream(self.device)
-            self.comm.wait_stream(compute)  # bands computed
+            self.comm.wait_stream(compute)  # previous epoch (and its ghosts) done
             with torch.cuda.stream(self.comm):
+                bands()
                 self._exchange_bands(self.b, lo, hi)
-            if inner[1] > inner[0]:
-                self.step(self.a, self.b, None, t, t, planes=inner, frame_ready=ready)
-                self.kernel_launches += per_call
+            interior()
             compute.wait_stream(self.comm)  # ghosts of the next epoch landed
         else:
+            bands()
             self._exchange_bands(self.b, lo, hi)
-            if inner[1] > inner[0]:
-                self.step(self.a, self.b, None, t, t, planes=inner, frame_ready=ready)
-                self.kernel_launches += per_call
+            interior()
         self._framed.add(self.b.data_ptr())
         self.overlapped_epochs += 1
 
