@@ -326,12 +326,20 @@ def main():
     from paper_2305_07390_b200 import _native, device
 
     rank, world, local = dist_env()
-    torch.cuda.set_device(local)
+    # (local % device_count: the single-GPU multi-rank smoke run of this path,
+    # EBISU_BENCH_BACKEND=gloo; one GPU per rank otherwise)
+    dev = local % max(1, torch.cuda.device_count())
+    torch.cuda.set_device(dev)
+    backend = os.environ.get("EBISU_BENCH_BACKEND", "nccl")
+    red_dev = "cuda" if backend == "nccl" else "cpu"  # gloo reduces host tensors
     dist = None
     if world > 1:
         import torch.distributed as dist
 
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=torch.device("cuda", dev))
+        else:
+            dist.init_process_group(backend)
     lib = _native.load()  # fails loudly without the native library
     st = eb.make_benchmark(STENCIL)
     stream = torch.cuda.current_stream()
@@ -364,7 +372,7 @@ def main():
     launches0 = runner.kernel_launches if world > 1 else 0
     if dist:
         dist.barrier()
-    sampler = ClockSampler(local)
+    sampler = ClockSampler(dev)
     sampler.start()
     time.sleep(0.3)
     ev0 = torch.cuda.Event(enable_timing=True)
@@ -383,7 +391,7 @@ def main():
     torch.cuda.synchronize()
     clocks = sampler.stop()
     ms = ev0.elapsed_time(ev1)
-    ms_t = torch.tensor([ms], device="cuda")
+    ms_t = torch.tensor([ms], device=red_dev)
     if dist:
         dist.barrier()
         dist.all_reduce(ms_t, op=dist.ReduceOp.MAX)
@@ -482,6 +490,37 @@ def main():
         line["configs"] = extra_configs(eb, device, _native, torch, stream, hbm_peak)
         c4 = line["configs"]["config4_j3d7pt_512"]
         line["config4_j3d7pt_512"] = c4  # (kept for round-1 readers)
+
+    if world > 1 and not args.no_3d:
+        # BASELINE config 5: j3d7pt fp64, 1024^3 per rank stacked on axis 0
+        # (weak scaling), slab-partitioned with the overlapped NCCL exchange;
+        # device time, max over ranks.  Guarded: a failure here is reported in
+        # the line instead of losing the headline measurement.
+        try:
+            st3 = eb.make_benchmark("j3d7pt")
+            run3 = edist.SlabSweep(st3, (1024 * world, 1024, 1024), t=4, seed=1, exact=True)
+            run3.run(8)  # warm-up (2 epochs)
+            torch.cuda.synchronize()
+            dist.barrier()
+            a3 = torch.cuda.Event(enable_timing=True)
+            b3 = torch.cuda.Event(enable_timing=True)
+            a3.record(stream)
+            run3.run(100)
+            b3.record(stream)
+            torch.cuda.synchronize()
+            t3 = torch.tensor([a3.elapsed_time(b3)], device=red_dev)
+            dist.all_reduce(t3, op=dist.ReduceOp.MAX)
+            ms3 = float(t3.item())
+            cells3 = run3.global_interior_cells() * 100
+            line["config5_weak_j3d7pt_1024_per_rank"] = {
+                "value": cells3 / (ms3 / 1e3) / 1e9, "unit": "GCells/s", "ms": ms3,
+                "time_steps": 100, "fused_depth_t": 4, "scaling": "weak",
+                "extents": [1024 * world, 1024, 1024],
+                "overlapped_epochs": run3.overlapped_epochs}
+            del run3
+            torch.cuda.empty_cache()
+        except Exception as exc:  # pragma: no cover - multi-GPU only
+            line["config5_weak_j3d7pt_1024_per_rank"] = {"error": repr(exc)[:300]}
 
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         line["cpu_baseline"] = cpu_oracle_sample()

@@ -58,3 +58,24 @@ def test_ours_arm_json_line():
     assert d["gpu_launches"] >= d["steps"]
     assert d["e2e"]["h2d_bytes_per_step"] > 0 and d["e2e"]["d2h_bytes_per_step"] > 0
     assert d["kernel"] == "stream2d_tb"
+
+
+@pytest.mark.gpu
+def test_multi_rank_bench_path_on_one_gpu():
+    """The N>1 bench path (torchrun, slab decomposition, overlapped epochs,
+    max-over-ranks timing, config-5 line) end to end: two ranks share one GPU
+    with gloo standing in for NCCL (EBISU_BENCH_BACKEND=gloo)."""
+    env = dict(os.environ, PYTHONPATH=ROOT, EBISU_BENCH_BACKEND="gloo")
+    r = subprocess.run([sys.executable, "-m", "torch.distributed.run", "--nnodes=1",
+                        "--nproc-per-node", "2", "--master-addr", "127.0.0.1",
+                        "--master-port", "29517", os.path.join(ROOT, "bench.py"), "--gpus", "2",
+                        "--steps", "1", "--warmup", "3", "--tsteps", "16"],
+                       capture_output=True, text=True, timeout=900, env=env)
+    assert r.returncode == 0, r.stderr[-2000:]
+    lines = [ln for ln in r.stdout.splitlines() if ln.strip().startswith("{")]
+    assert len(lines) == 1, r.stdout
+    d = json.loads(lines[0])
+    assert d["n_gpus"] == 2 and d["value"] > 0 and d["scaling"] == "weak"
+    assert d["gpu_launches"] > 0
+    c5 = d["config5_weak_j3d7pt_1024_per_rank"]
+    assert "error" not in c5 and c5["value"] > 0 and c5["overlapped_epochs"] > 0
