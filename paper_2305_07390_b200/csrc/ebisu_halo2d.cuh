@@ -82,7 +82,7 @@ struct Halo2DArgs {
 };
 
 // One unit: CTA strip x row segment.  EDGE: the strip touches a frame column.
-template <class SH, int T, int C, int NW, int S, bool EXACT, bool UNI, bool EDGE, bool SHIFT>
+template <class SH, int T, int C, int NW, int S, bool EXACT, bool UNI, bool EDGE, int SHIFT>
 __device__ __forceinline__ int halo2d_unit(const CUtensorMap* tm, double* __restrict__ out,
                                            double* ring, uint64_t* bars, double* xh,
                                            uint64_t* advbar, uint32_t ring_cnt, uint32_t& adv,
@@ -94,8 +94,9 @@ __device__ __forceinline__ int halo2d_unit(const CUtensorMap* tm, double* __rest
   constexpr int TZ = T * Z;
 
   const int ka = max(0, r0 - T * R);
-  // SHIFT: shifted windows, one advance per block (see stream2d_unit)
-  constexpr int UW = SHIFT ? 1 : W;
+  // SHIFT = U > 0: shifted windows, U advances per block (see stream2d_unit)
+  constexpr int UW = SHIFT ? SHIFT : W;
+  constexpr int WS = SHIFT ? W + SHIFT - 1 : W;
   const int nadv = (r1 + TZ - ka + UW - 1) / UW * UW;  // whole unrolled blocks
   const int kend = ka + nadv;
   const int XW = X0 + warp * LC;  // this warp's first column
@@ -121,11 +122,11 @@ __device__ __forceinline__ int halo2d_unit(const CUtensorMap* tm, double* __rest
     stmask |= (uint32_t)st << c;
   }
 
-  double win[T][W][C];
+  double win[T][WS][C];
 #pragma unroll
   for (int s = 0; s < T; ++s)
 #pragma unroll
-    for (int w = 0; w < W; ++w)
+    for (int w = 0; w < WS; ++w)
 #pragma unroll
       for (int c = 0; c < C; ++c) win[s][w][c] = 0.0;
 
@@ -180,13 +181,10 @@ __device__ __forceinline__ int halo2d_unit(const CUtensorMap* tm, double* __rest
         }
 #pragma unroll
         for (int c = 0; c < C; ++c) {
-          if constexpr (SHIFT) {
-#pragma unroll
-            for (int w = 0; w + 1 < W; ++w) win[0][w][c] = win[0][w + 1][c];
-            win[0][W - 1][c] = v[c];
-          } else {
+          if constexpr (SHIFT)
+            win[0][W - 1 + uu][c] = v[c];
+          else
             win[0][uu][c] = v[c];
-          }
         }
         push(0, bk, v);
       }
@@ -198,7 +196,7 @@ __device__ __forceinline__ int halo2d_unit(const CUtensorMap* tm, double* __rest
         static_for<2 * R + 1>([&](auto dI) {
           constexpr int dy = decltype(dI)::value - R;
           if constexpr (row_has_halo<SH>(dy)) {
-            const int sl = SHIFT ? R + dy : pmod<W>(uu - s * Z + dy);
+            const int sl = SHIFT ? R + dy + uu : pmod<W>(uu - s * Z + dy);
             const int xs = (k - Z + dy) & (NB - 1);  // advance that produced the row
             const double* Lb = xrow(s - 1, xs, wr, 0);   // right neighbour's left edge
             const double* Rb = xrow(s - 1, xs, wl, 1);   // left neighbour's right edge
@@ -227,7 +225,7 @@ __device__ __forceinline__ int halo2d_unit(const CUtensorMap* tm, double* __rest
           constexpr Off o = SH::tap(i);
 #pragma unroll
           for (int c = 0; c < C; ++c) {
-            const int sl = SHIFT ? R + o.d0 : pmod<W>(uu - s * Z + o.d0);
+            const int sl = SHIFT ? R + o.d0 + uu : pmod<W>(uu - s * Z + o.d0);
             const int cc = c + o.d1;
             double x;
             if (cc < 0)
@@ -249,7 +247,7 @@ __device__ __forceinline__ int halo2d_unit(const CUtensorMap* tm, double* __rest
         double nv[C];
 #pragma unroll
         for (int c = 0; c < C; ++c) {
-          const double centre = win[s - 1][SHIFT ? R : pmod<W>(uu - s * Z)][c];
+          const double centre = win[s - 1][SHIFT ? R + uu : pmod<W>(uu - s * Z)][c];
           const double val = (UNI && s < T) ? __dmul_rn(cf.c[0], acc[c]) : acc[c];
           if constexpr (EDGE || FROWS) {
             bool f = frow;
@@ -262,13 +260,10 @@ __device__ __forceinline__ int halo2d_unit(const CUtensorMap* tm, double* __rest
         if constexpr (s < T) {
 #pragma unroll
           for (int c = 0; c < C; ++c) {
-            if constexpr (SHIFT) {
-#pragma unroll
-              for (int w = 0; w + 1 < W; ++w) win[s][w][c] = win[s][w + 1][c];
-              win[s][W - 1][c] = nv[c];
-            } else {
+            if constexpr (SHIFT)
+              win[s][W - 1 + uu][c] = nv[c];
+            else
               win[s][pmod<W>(uu - s * Z)][c] = nv[c];
-            }
           }
           push(s, bk, nv);
         } else {
@@ -286,6 +281,15 @@ __device__ __forceinline__ int halo2d_unit(const CUtensorMap* tm, double* __rest
       if (lane == 0) mbar_arrive(&advbar[adv % Cfg::DR]);  // release covers the warp
       ++adv;
     }
+    if constexpr (SHIFT) {
+      // keep the W-1 newest rows of every level for the next block
+#pragma unroll
+      for (int L = 0; L < T; ++L)
+#pragma unroll
+        for (int w = 0; w + 1 < W; ++w)
+#pragma unroll
+          for (int c = 0; c < C; ++c) win[L][w][c] = win[L][w + SHIFT][c];
+    }
   };
 
   for (int kbase = ka; kbase < kend; kbase += UW) {
@@ -299,7 +303,7 @@ __device__ __forceinline__ int halo2d_unit(const CUtensorMap* tm, double* __rest
 }
 
 template <class SH, int T, int C, int NW, int S, bool EXACT, bool UNI, int MINB,
-          bool SHIFT = false>
+          int SHIFT = 0>
 __global__ void __launch_bounds__(NW * 32, MINB)
     k_halo2d(const __grid_constant__ TmapSet maps, const Halo2DArgs a,
              const __grid_constant__ Coefs<SH::NT> cf) {

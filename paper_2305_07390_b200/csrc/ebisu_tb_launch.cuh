@@ -134,7 +134,7 @@ cudaError_t launch_stream3d(const TbLaunch& L) {
   }
 
 template <class SH, int T, int C, int NW, int S, bool EXACT, bool UNI, int MINB,
-          bool SHIFT = false>
+          int SHIFT = 0>
 cudaError_t launch_halo2d(const TbLaunch& L) {
   using Cfg = Halo2DCfg<SH, T, C, NW, S>;
   auto kern = k_halo2d<SH, T, C, NW, S, EXACT, UNI, MINB, SHIFT>;
@@ -171,7 +171,7 @@ cudaError_t launch_halo2d(const TbLaunch& L) {
 // box0 = warp columns (TMA box), valid_x = valid columns per CTA strip, C =
 // cells per lane, z = level skew, wn = strip columns (LW)
 #define EBISU_H2D_ENTRY(SHAPE_ID, SH, T, C, NW, S, EX, UNI, MINB) \
-  EBISU_H2D_ENTRY_SH(SHAPE_ID, SH, T, C, NW, S, EX, UNI, MINB, false)
+  EBISU_H2D_ENTRY_SH(SHAPE_ID, SH, T, C, NW, S, EX, UNI, MINB, 0)
 #define EBISU_H2D_ENTRY_SH(SHAPE_ID, SH, T, C, NW, S, EX, UNI, MINB, SHIFT)                    \
   TbKernel {                                                                                  \
     SHAPE_ID, 2, T, C, NW, S, EX, UNI, Halo2DCfg<SH, T, C, NW, S>::SMEM_BYTES, 32 * C, 1, 1,   \
