@@ -650,7 +650,8 @@ int run_tb3d_stage(const ProblemDesc& p, const TbKernel* k, int epochs, int firs
   // EBISU_SEG3D=uniform: the balanced uniform length, for A/B measurement)
   const char* seg_mode = getenv("EBISU_SEG3D");
   const bool uniform = seg_mode && strcmp(seg_mode, "uniform") == 0;
-  const int min_len = std::max(std::max(8, 2 * T * R), 4 * (T * R + T * k->z));
+  int min_len = std::max(std::max(8, 2 * T * R), 4 * (T * R + T * k->z));
+  if (const char* v = getenv("EBISU_SEGMIN3D")) min_len = std::max(8, atoi(v));  // tuning
   const std::vector<int> seg_start =
       guided_segments(p.z_lo, p.z_hi, tiles, max_ctas, seg_len,
                       uniform ? std::max(seg_len, min_len) : min_len,
