@@ -153,7 +153,7 @@ __host__ __device__ constexpr int pmod(int a) {
 // One work unit (warp strip x row segment) of one epoch.  FC selects the
 // frame-column handling (see StripGeom); frame rows are handled per block.
 template <class SH, int T, int C, int S, bool EXACT, bool UNI, int FC, class E, int SHIFT = 0>
-__device__ __forceinline__ void stream2d_unit(const CUtensorMap* tm, E* __restrict__ out,
+__device__ __forceinline__ int stream2d_unit(const CUtensorMap* tm, E* __restrict__ out,
                                               E* ring, uint64_t* bars, uint32_t ring_cnt,
                                               int lane, int n0, int n1, const StripGeom& g,
                                               int r0, int r1, const Coefs<SH::NT, E>& cf) {
@@ -166,12 +166,16 @@ __device__ __forceinline__ void stream2d_unit(const CUtensorMap* tm, E* __restri
 
   const int X0 = g.X0;
   const int ka = max(0, r0 - TR);
-  const int kb = min(n0, r1 + TR);
   const int kend = r1 + TR;
+  // rows [ka, kload) are all loaded (whole unrolled blocks): TMA zero-fills
+  // rows >= n0, and rows >= r1 + T*R only feed target rows >= r1, which are
+  // never stored -- so the level-0 read needs no branch
+  constexpr int UWC = SHIFT ? SHIFT : 2 * R + 1;
+  const int kload = ka + (kend - ka + UWC - 1) / UWC * UWC;
 
   // Prologue: fill the ring S rows ahead.
   if (lane == 0) {
-    for (int i = 0; i < S && ka + i < kb; ++i) {
+    for (int i = 0; i < S && ka + i < kload; ++i) {
       const uint32_t slot = (ring_cnt + i) & (S - 1);
       mbar_arrive_expect_tx(&bars[slot], ROW_BYTES);
       tma_load_2d(ring + slot * LC, tm, X0, ka + i, &bars[slot]);
@@ -244,14 +248,14 @@ __device__ __forceinline__ void stream2d_unit(const CUtensorMap* tm, E* __restri
       // row never stays live across the advance)
       {
         E v[C];
-        if (k < kb) {
+        {
           const uint32_t pos = ring_cnt + (uint32_t)(k - ka);
           const uint32_t slot = pos & (S - 1);
           mbar_wait(&bars[slot], (pos / S) & 1);
           // Refill the slot consumed one advance ago: its LDS results have
           // been used by now, so the async-proxy write cannot overtake the
           // generic-proxy read (no proxy fence on the hot path).
-          if (lane == 0 && k > ka && k - 1 + S < kb) {
+          if (lane == 0 && k > ka && k - 1 + S < kload) {
             const uint32_t ps = (pos - 1) & (S - 1);
             mbar_arrive_expect_tx(&bars[ps], ROW_BYTES);
             tma_load_2d(ring + ps * LC, tm, X0, k - 1 + S, &bars[ps]);
@@ -268,9 +272,6 @@ __device__ __forceinline__ void stream2d_unit(const CUtensorMap* tm, E* __restri
 #pragma unroll
             for (int c = 0; c < C; ++c) v[c] = rowp[c];
           }
-        } else {
-#pragma unroll
-          for (int c = 0; c < C; ++c) v[c] = 0.0;
         }
         // UNI: the window holds products y = c*x (one DMUL per cell per level)
 #pragma unroll
@@ -386,6 +387,7 @@ __device__ __forceinline__ void stream2d_unit(const CUtensorMap* tm, E* __restri
     else
       block(kbase, std::false_type{});
   }
+  return kload - ka;
 }
 
 // Warp-wide atomic grab of the next work unit (lane 0 increments).
@@ -460,33 +462,32 @@ __global__ void __launch_bounds__(NW * 32, MINB)
         __syncwarp();
         fence_proxy_async_global();  // the TMA loads below see those stores
       }
-      const int ka = max(0, r0 - TR);
-      const int kb = min(n0, r1 + TR);
       long long t_start = 0;
       if (a.unit_clock && e == 0 && lane == 0)
         asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_start));
+      int used;
       if constexpr (R > C) {
-        stream2d_unit<SH, T, C, S, EXACT, UNI, 3, E, SHIFT>(tm, out, ring, bars, ring_cnt, lane, n0, n1, g, r0,
-                                             r1, cf);
+        used = stream2d_unit<SH, T, C, S, EXACT, UNI, 3, E, SHIFT>(tm, out, ring, bars, ring_cnt,
+                                                                   lane, n0, n1, g, r0, r1, cf);
       } else switch (g.fc) {
         case 0:
-          stream2d_unit<SH, T, C, S, EXACT, UNI, 0, E, SHIFT>(tm, out, ring, bars, ring_cnt, lane, n0, n1, g,
-                                               r0, r1, cf);
+          used = stream2d_unit<SH, T, C, S, EXACT, UNI, 0, E, SHIFT>(tm, out, ring, bars, ring_cnt,
+                                                                     lane, n0, n1, g, r0, r1, cf);
           break;
         case 1:
-          stream2d_unit<SH, T, C, S, EXACT, UNI, 1, E, SHIFT>(tm, out, ring, bars, ring_cnt, lane, n0, n1, g,
-                                               r0, r1, cf);
+          used = stream2d_unit<SH, T, C, S, EXACT, UNI, 1, E, SHIFT>(tm, out, ring, bars, ring_cnt,
+                                                                     lane, n0, n1, g, r0, r1, cf);
           break;
         case 2:
-          stream2d_unit<SH, T, C, S, EXACT, UNI, 2, E, SHIFT>(tm, out, ring, bars, ring_cnt, lane, n0, n1, g,
-                                               r0, r1, cf);
+          used = stream2d_unit<SH, T, C, S, EXACT, UNI, 2, E, SHIFT>(tm, out, ring, bars, ring_cnt,
+                                                                     lane, n0, n1, g, r0, r1, cf);
           break;
         default:
-          stream2d_unit<SH, T, C, S, EXACT, UNI, 3, E, SHIFT>(tm, out, ring, bars, ring_cnt, lane, n0, n1, g,
-                                               r0, r1, cf);
+          used = stream2d_unit<SH, T, C, S, EXACT, UNI, 3, E, SHIFT>(tm, out, ring, bars, ring_cnt,
+                                                                     lane, n0, n1, g, r0, r1, cf);
           break;
       }
-      ring_cnt += (uint32_t)(kb - ka);
+      ring_cnt += (uint32_t)used;
       if (a.flags) {
         // publish: every lane's stores, then the flag (release)
         fence_proxy_async_global();
