@@ -493,34 +493,38 @@ def main():
 
     if world > 1 and not args.no_3d:
         # BASELINE config 5: j3d7pt fp64, 1024^3 per rank stacked on axis 0
-        # (weak scaling), slab-partitioned with the overlapped NCCL exchange;
-        # device time, max over ranks.  Guarded: a failure here is reported in
-        # the line instead of losing the headline measurement.
-        try:
-            st3 = eb.make_benchmark("j3d7pt")
-            run3 = edist.SlabSweep(st3, (1024 * world, 1024, 1024), t=4, seed=1, exact=True)
-            run3.run(8)  # warm-up (2 epochs)
-            torch.cuda.synchronize()
-            dist.barrier()
-            a3 = torch.cuda.Event(enable_timing=True)
-            b3 = torch.cuda.Event(enable_timing=True)
-            a3.record(stream)
-            run3.run(100)
-            b3.record(stream)
-            torch.cuda.synchronize()
-            t3 = torch.tensor([a3.elapsed_time(b3)], device=red_dev)
-            dist.all_reduce(t3, op=dist.ReduceOp.MAX)
-            ms3 = float(t3.item())
-            cells3 = run3.global_interior_cells() * 100
-            line["config5_weak_j3d7pt_1024_per_rank"] = {
-                "value": cells3 / (ms3 / 1e3) / 1e9, "unit": "GCells/s", "ms": ms3,
-                "time_steps": 100, "fused_depth_t": 4, "scaling": "weak",
-                "extents": [1024 * world, 1024, 1024],
-                "overlapped_epochs": run3.overlapped_epochs}
-            del run3
-            torch.cuda.empty_cache()
-        except Exception as exc:  # pragma: no cover - multi-GPU only
-            line["config5_weak_j3d7pt_1024_per_rank"] = {"error": repr(exc)[:300]}
+        # (weak scaling) and 1024^3 in total (strong scaling), slab-partitioned
+        # with the overlapped NCCL exchange; device time, max over ranks.
+        # Guarded: a failure here is reported in the line instead of losing the
+        # headline measurement.
+        def config5(extents, key, scaling):
+            try:
+                st3 = eb.make_benchmark("j3d7pt")
+                run3 = edist.SlabSweep(st3, extents, t=4, seed=1, exact=True)
+                run3.run(8)  # warm-up (2 epochs)
+                torch.cuda.synchronize()
+                dist.barrier()
+                a3 = torch.cuda.Event(enable_timing=True)
+                b3 = torch.cuda.Event(enable_timing=True)
+                a3.record(stream)
+                run3.run(100)
+                b3.record(stream)
+                torch.cuda.synchronize()
+                t3 = torch.tensor([a3.elapsed_time(b3)], device=red_dev)
+                dist.all_reduce(t3, op=dist.ReduceOp.MAX)
+                ms3 = float(t3.item())
+                cells3 = run3.global_interior_cells() * 100
+                line[key] = {
+                    "value": cells3 / (ms3 / 1e3) / 1e9, "unit": "GCells/s", "ms": ms3,
+                    "time_steps": 100, "fused_depth_t": 4, "scaling": scaling,
+                    "extents": list(extents), "overlapped_epochs": run3.overlapped_epochs}
+                del run3
+                torch.cuda.empty_cache()
+            except Exception as exc:  # pragma: no cover - multi-GPU only
+                line[key] = {"error": repr(exc)[:300]}
+
+        config5((1024 * world, 1024, 1024), "config5_weak_j3d7pt_1024_per_rank", "weak")
+        config5((1024, 1024, 1024), "config5_strong_j3d7pt_1024_total", "strong")
 
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         line["cpu_baseline"] = cpu_oracle_sample()

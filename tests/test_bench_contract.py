@@ -77,5 +77,6 @@ def test_multi_rank_bench_path_on_one_gpu():
     d = json.loads(lines[0])
     assert d["n_gpus"] == 2 and d["value"] > 0 and d["scaling"] == "weak"
     assert d["gpu_launches"] > 0
-    c5 = d["config5_weak_j3d7pt_1024_per_rank"]
-    assert "error" not in c5 and c5["value"] > 0 and c5["overlapped_epochs"] > 0
+    for key in ("config5_weak_j3d7pt_1024_per_rank", "config5_strong_j3d7pt_1024_total"):
+        c5 = d[key]
+        assert "error" not in c5 and c5["value"] > 0 and c5["overlapped_epochs"] > 0, c5
