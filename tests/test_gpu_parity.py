@@ -482,3 +482,26 @@ def test_2d_every_registered_variant_bitwise(name):
                     if ref is None:
                         ref = oracle_run(g.cells, taps_of(st), steps)
                     assert np.array_equal(out.cells, ref), (name, t, v, scheme, ext, tr)
+
+
+def test_concurrent_calls_from_threads():
+    """The reference promises pure, thread-safe calls: host
+    sweeps issued from several Python threads at once all return the oracle's
+    answer and leave their inputs untouched."""
+    from concurrent.futures import ThreadPoolExecutor
+
+    cases = [("j2d5pt", (200, 260), 9), ("j3d7pt", (30, 40, 66), 6),
+             ("j2d9pt", (150, 200), 7), ("j3d27pt", (20, 30, 34), 4)] * 2
+    grids = [eb.random_grid(ext, 300 + i) for i, (_, ext, _) in enumerate(cases)]
+    before = [g.cells.copy() for g in grids]
+
+    def run(i):
+        name, _, steps = cases[i]
+        return eb.reference_run(grids[i], _shape(name), steps)
+
+    with ThreadPoolExecutor(max_workers=4) as ex:
+        outs = list(ex.map(run, range(len(cases))))
+    for i, (name, _, steps) in enumerate(cases):
+        assert np.array_equal(grids[i].cells, before[i])
+        ref = oracle_run(before[i], taps_of(_shape(name)), steps)
+        assert np.array_equal(outs[i].cells, ref), (name, i)
