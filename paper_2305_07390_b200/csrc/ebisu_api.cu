@@ -73,6 +73,7 @@ int identify_shape(const ebisu_stencil* s) {
   if (match_shape<NoCornerShape3<true>>(s)) return SHAPE_J3D17PT;
   if (match_shape<BoxShape<3, 1>>(s)) return SHAPE_J3D27PT;
   if (match_shape<NoCornerShape3<false>>(s)) return SHAPE_POISSON;
+  if (match_shape<StarShape<1, 1>>(s)) return SHAPE_J1D3PT;
   return SHAPE_GENERIC;
 }
 
@@ -469,7 +470,8 @@ int run_tb2d_stage(const ProblemDesc& p, const TbKernel* k, int epochs, int firs
     L.flags = flags;
     EB_CUDA(k->launch(L));
     ctr->launches += 1;
-    ctr->syncs_device += (uint64_t)(epochs - 1);
+    // dataflow epochs replace the grid-wide barrier by per-unit flag waits
+    if (!flags) ctr->syncs_device += (uint64_t)(epochs - 1);
   } else {
     int src = first_src, dst = first_dst;
     for (int e = 0; e < epochs; ++e) {
@@ -819,9 +821,12 @@ int run_device_impl(const ProblemDesc& p0, const void* d_in, void* d_out, void* 
   // ping-pong buffers (a shell of 2R planes/rows/columns, not the grid).
   bool any_uni = false;
   for (auto& s : stages) any_uni = any_uni || (s.k && s.k->uni);
-  if (any_uni && !(prm && prm->frame_ready)) {
+  if (any_uni) {
     for (int b = BUF_OUT; b <= BUF_SCR; ++b) {
       if (!bufs[b]) continue;
+      // frame_ready vouches for the caller's buffers only: scratch the
+      // library just allocated holds no frame yet
+      if (prm && prm->frame_ready && !(b == BUF_SCR && own_scr)) continue;
       cudaError_t e = launch_frame_copy(p, d_in, bufs[b], st, di.sms);
       if (e != cudaSuccess) {
         if (own_scr) cudaFreeAsync(scr, st);
@@ -954,6 +959,8 @@ static int32_t run_device_entry(const ebisu_stencil* stencil, int32_t ndim,
                                 void* stream, ebisu_trace* trace, int elem) {
   g_err.clear();
   if (steps < 0) return fail(EBISU_ERR_VALUE, "step count must be >= 0");
+  if (steps > INT32_MAX)
+    return fail(EBISU_ERR_VALUE, "step count %lld exceeds 2^31-1", (long long)steps);
   ProblemDesc p;
   int rc = validate(stencil, ndim, extents, params, &p);
   if (rc) return rc;
@@ -991,6 +998,8 @@ static int32_t run_host_entry(const ebisu_stencil* stencil, int32_t ndim,
                               const ebisu_params* params, ebisu_trace* trace, int elem) {
   g_err.clear();
   if (steps < 0) return fail(EBISU_ERR_VALUE, "step count must be >= 0");
+  if (steps > INT32_MAX)
+    return fail(EBISU_ERR_VALUE, "step count %lld exceeds 2^31-1", (long long)steps);
   ProblemDesc p;
   int rc = validate(stencil, ndim, extents, params, &p);
   if (rc) return rc;

@@ -6,91 +6,188 @@
 // (16 B/cell-step), the path for arbitrary user stencils that match no
 // specialised kernel, and the remainder steps of a sweep when T is not a
 // multiple of the fused depth and no matching depth was instantiated.
+#include <type_traits>
+
 #include "ebisu_common.cuh"
 #include "ebisu_internal.h"
+#include "ebisu_shapes.cuh"
 
 namespace ebisu {
 
+// Geometry of one naive step: the grid as P planes x Y rows x X cells (1-D:
+// P = Y = 1; 2-D: P = 1), rows [row_lo, row_hi) written.  A row is the unit of
+// work: a CTA owns CPT*BS consecutive cells of one row, so every index is a
+// row base plus a lane offset -- no per-cell 64-bit division -- and each
+// thread keeps CPT independent cells (CPT*ntaps independent loads) in flight.
+struct NaiveGeom {
+  long long P, Y, X;
+  long long row_lo, row_hi;
+  int R0, R1, R2;     // frame widths along the three padded axes
+  int chunks;         // CTAs per row
+};
+
 struct NaiveTaps {
   int ntaps;
-  int rad;
-  int dims;
-  long long n0, n1, n2;  // extents (unused axes = 1)
-  long long z_lo, z_hi;  // output planes [z_lo, z_hi) along axis 0
   long long lin[EBISU_MAX_TAPS];  // linear offsets
   double coef[EBISU_MAX_TAPS];
 };
 
-template <bool EXACT, class E>
-__global__ void __launch_bounds__(256) k_naive_step(const E* __restrict__ in,
-                                                    E* __restrict__ out,
-                                                    const __grid_constant__ NaiveTaps tp) {
-  const long long plane = tp.n1 * tp.n2;
-  const long long base = tp.z_lo * plane;
-  const long long total = (tp.z_hi - tp.z_lo) * plane;
-  const long long stride = (long long)gridDim.x * blockDim.x;
-  for (long long idx = base + (long long)blockIdx.x * blockDim.x + threadIdx.x;
-       idx < base + total; idx += stride) {
-    const long long i2 = idx % tp.n2;
-    const long long r = idx / tp.n2;
-    const long long i1 = r % tp.n1;
-    const long long i0 = r / tp.n1;
-    const int R = tp.rad;
-    bool frame = (i0 < R) || (i0 >= tp.n0 - R);
-    if (tp.dims >= 2) frame |= (i1 < R) || (i1 >= tp.n1 - R);
-    if (tp.dims >= 3) frame |= (i2 < R) || (i2 >= tp.n2 - R);
-    E v;
-    if (frame) {
-      v = in[idx];
-    } else {
-      v = tap_first<EXACT, E>((E)tp.coef[0], __ldg(in + idx + tp.lin[0]));
-      for (int t = 1; t < tp.ntaps; ++t)
-        v = tap_next<EXACT, E>(v, (E)tp.coef[t], __ldg(in + idx + tp.lin[t]));
+constexpr int kNaiveBS = 256;  // threads per CTA
+constexpr int kNaiveCPT = 4;   // cells per thread (strided by kNaiveBS: coalesced)
+
+// Compile-time tap pattern (catalog shapes, ebisu_shapes.cuh) or runtime taps
+// (SH = void: any stencil, any order).  EXACT: one rounding per multiply and
+// per add in tap order (bitwise equal to apply_taps, grid.py:76-93).
+template <class SH, bool EXACT, class E>
+__global__ void __launch_bounds__(kNaiveBS) k_naive_step(const E* __restrict__ in,
+                                                         E* __restrict__ out,
+                                                         const __grid_constant__ NaiveGeom g,
+                                                         const __grid_constant__ NaiveTaps tp) {
+  const long long row = g.row_lo + (long long)(blockIdx.x / (unsigned)g.chunks);
+  const int chunk = (int)(blockIdx.x % (unsigned)g.chunks);
+  if (row >= g.row_hi) return;
+  const long long p = row / g.Y, y = row - p * g.Y;
+  const E* src = in + row * g.X;
+  E* dst = out + row * g.X;
+  const long long x0 = (long long)chunk * (kNaiveBS * kNaiveCPT) + threadIdx.x;
+  const bool frame_row = (p < g.R0) || (p >= g.P - g.R0) || (y < g.R1) || (y >= g.Y - g.R1);
+  if (frame_row) {
+#pragma unroll
+    for (int k = 0; k < kNaiveCPT; ++k) {
+      const long long x = x0 + k * kNaiveBS;
+      if (x < g.X) dst[x] = src[x];
     }
-    out[idx] = v;
+    return;
+  }
+  E acc[kNaiveCPT];
+  bool live[kNaiveCPT], inner[kNaiveCPT];
+#pragma unroll
+  for (int k = 0; k < kNaiveCPT; ++k) {
+    const long long x = x0 + k * kNaiveBS;
+    live[k] = x < g.X;
+    inner[k] = (x >= g.R2) && (x < g.X - g.R2);
+  }
+  if constexpr (!std::is_void_v<SH>) {
+    // catalog shape: every tap's offset is a compile-time (d0, d1, d2) over
+    // runtime strides; all NT*CPT loads are independent of the sums
+    const long long plane = g.Y * g.X;
+    static_for<SH::NT>([&](auto iI) {
+      constexpr int i = decltype(iI)::value;
+      constexpr Off o = SH::tap(i);
+      long long lin;
+      if constexpr (SH::dims == 3)
+        lin = o.d0 * plane + o.d1 * g.X + o.d2;
+      else if constexpr (SH::dims == 2)
+        lin = o.d0 * g.X + o.d1;
+      else
+        lin = o.d0;
+      const E c = (E)tp.coef[i];
+#pragma unroll
+      for (int k = 0; k < kNaiveCPT; ++k) {
+        const long long x = x0 + k * kNaiveBS;
+        const E v = inner[k] ? __ldg(src + x + lin) : (E)0;
+        if constexpr (i == 0)
+          acc[k] = tap_first<EXACT, E>(c, v);
+        else
+          acc[k] = tap_next<EXACT, E>(acc[k], c, v);
+      }
+    });
+  } else {
+#pragma unroll
+    for (int k = 0; k < kNaiveCPT; ++k) {
+      const long long x = x0 + k * kNaiveBS;
+      acc[k] = tap_first<EXACT, E>((E)tp.coef[0], inner[k] ? __ldg(src + x + tp.lin[0]) : (E)0);
+    }
+    for (int t = 1; t < tp.ntaps; ++t) {
+      const long long lin = tp.lin[t];
+      const E c = (E)tp.coef[t];
+#pragma unroll
+      for (int k = 0; k < kNaiveCPT; ++k) {
+        const long long x = x0 + k * kNaiveBS;
+        acc[k] = tap_next<EXACT, E>(acc[k], c, inner[k] ? __ldg(src + x + lin) : (E)0);
+      }
+    }
+  }
+#pragma unroll
+  for (int k = 0; k < kNaiveCPT; ++k) {
+    const long long x = x0 + k * kNaiveBS;
+    if (live[k]) dst[x] = inner[k] ? acc[k] : src[x];
+  }
+}
+
+template <class SH, class E>
+cudaError_t launch_naive_typed(const E* in, E* out, const NaiveGeom& g, const NaiveTaps& tp,
+                               bool exact, long long blocks, cudaStream_t st) {
+  if (exact)
+    k_naive_step<SH, true, E><<<(unsigned)blocks, kNaiveBS, 0, st>>>(in, out, g, tp);
+  else
+    k_naive_step<SH, false, E><<<(unsigned)blocks, kNaiveBS, 0, st>>>(in, out, g, tp);
+  return cudaGetLastError();
+}
+
+template <class E>
+cudaError_t launch_naive_shape(int shape_id, const E* in, E* out, const NaiveGeom& g,
+                               const NaiveTaps& tp, bool exact, long long blocks,
+                               cudaStream_t st) {
+  switch (shape_id) {
+    case SHAPE_J2D5PT: return launch_naive_typed<StarShape<2, 1>>(in, out, g, tp, exact, blocks, st);
+    case SHAPE_J2D9PT: return launch_naive_typed<StarShape<2, 2>>(in, out, g, tp, exact, blocks, st);
+    case SHAPE_J2D9PT_GOL:
+      return launch_naive_typed<BoxShape<2, 1>>(in, out, g, tp, exact, blocks, st);
+    case SHAPE_J2D25PT: return launch_naive_typed<BoxShape<2, 2>>(in, out, g, tp, exact, blocks, st);
+    case SHAPE_J2D13PT: return launch_naive_typed<StarShape<2, 3>>(in, out, g, tp, exact, blocks, st);
+    case SHAPE_J2DS25PT:
+      return launch_naive_typed<StarShape<2, 6>>(in, out, g, tp, exact, blocks, st);
+    case SHAPE_J3D7PT: return launch_naive_typed<StarShape<3, 1>>(in, out, g, tp, exact, blocks, st);
+    case SHAPE_J3D13PT: return launch_naive_typed<StarShape<3, 2>>(in, out, g, tp, exact, blocks, st);
+    case SHAPE_J3D17PT:
+      return launch_naive_typed<NoCornerShape3<true>>(in, out, g, tp, exact, blocks, st);
+    case SHAPE_J3D27PT: return launch_naive_typed<BoxShape<3, 1>>(in, out, g, tp, exact, blocks, st);
+    case SHAPE_POISSON:
+      return launch_naive_typed<NoCornerShape3<false>>(in, out, g, tp, exact, blocks, st);
+    case SHAPE_J1D3PT: return launch_naive_typed<StarShape<1, 1>>(in, out, g, tp, exact, blocks, st);
+    default: return launch_naive_typed<void>(in, out, g, tp, exact, blocks, st);
   }
 }
 
 cudaError_t launch_naive_step(const ProblemDesc& p, const void* in, void* out,
                               bool exact, cudaStream_t st, int num_sms) {
+  (void)num_sms;
+  NaiveGeom g{};
   NaiveTaps tp{};
   tp.ntaps = p.ntaps;
-  tp.rad = p.rad;
-  tp.dims = p.dims;
-  tp.n0 = p.ext[0];
-  tp.n1 = p.dims >= 2 ? p.ext[1] : 1;
-  tp.n2 = p.dims >= 3 ? p.ext[2] : 1;
-  tp.z_lo = p.z_lo;
-  tp.z_hi = p.z_hi > 0 ? p.z_hi : p.ext[0];
+  g.P = p.dims == 3 ? p.ext[0] : 1;
+  g.Y = p.dims == 3 ? p.ext[1] : (p.dims == 2 ? p.ext[0] : 1);
+  g.X = p.ext[p.dims - 1];
+  g.R0 = p.dims == 3 ? p.rad : 0;
+  g.R1 = p.dims >= 2 ? p.rad : 0;
+  g.R2 = p.rad;
+  const long long z_hi = p.z_hi > 0 ? p.z_hi : p.ext[0];
+  const long long per = p.dims == 3 ? g.Y : 1;  // rows per axis-0 index
+  g.row_lo = p.dims == 1 ? 0 : (long long)p.z_lo * per;
+  g.row_hi = p.dims == 1 ? 1 : z_hi * per;
+  g.chunks = (int)((g.X + kNaiveBS * kNaiveCPT - 1) / (kNaiveBS * kNaiveCPT));
+  const long long plane = g.Y * g.X;
   for (int t = 0; t < p.ntaps; ++t) {
     const int* o = p.offsets + t * p.dims;
-    long long l = o[0];
-    if (p.dims >= 2) l = l * tp.n1 + o[1];
-    if (p.dims >= 3) l = l * tp.n2 + o[2];
+    long long l;
+    if (p.dims == 3)
+      l = o[0] * plane + (long long)o[1] * g.X + o[2];
+    else if (p.dims == 2)
+      l = (long long)o[0] * g.X + o[1];
+    else
+      l = o[0];
     tp.lin[t] = l;
     tp.coef[t] = p.coeffs[t];
   }
-  const long long total = (tp.z_hi - tp.z_lo) * tp.n1 * tp.n2;
-  long long blocks = (total + 255) / 256;
-  const long long cap = (long long)num_sms * 8;
-  if (blocks > cap) blocks = cap;
-  if (blocks < 1) blocks = 1;
-  if (p.elem == 4) {
-    const float* fi = static_cast<const float*>(in);
-    float* fo = static_cast<float*>(out);
-    if (exact)
-      k_naive_step<true, float><<<(unsigned)blocks, 256, 0, st>>>(fi, fo, tp);
-    else
-      k_naive_step<false, float><<<(unsigned)blocks, 256, 0, st>>>(fi, fo, tp);
-  } else {
-    const double* di = static_cast<const double*>(in);
-    double* dout = static_cast<double*>(out);
-    if (exact)
-      k_naive_step<true, double><<<(unsigned)blocks, 256, 0, st>>>(di, dout, tp);
-    else
-      k_naive_step<false, double><<<(unsigned)blocks, 256, 0, st>>>(di, dout, tp);
-  }
-  return cudaGetLastError();
+  const long long blocks = (g.row_hi - g.row_lo) * g.chunks;
+  if (blocks <= 0) return cudaSuccess;
+  if (blocks > 0x7fffffffll) return cudaErrorInvalidValue;
+  if (p.elem == 4)
+    return launch_naive_shape<float>(p.shape_id, static_cast<const float*>(in),
+                                     static_cast<float*>(out), g, tp, exact, blocks, st);
+  return launch_naive_shape<double>(p.shape_id, static_cast<const double*>(in),
+                                    static_cast<double*>(out), g, tp, exact, blocks, st);
 }
 
 // ---- frame pre-copy -----------------------------------------------------------

@@ -86,7 +86,8 @@ enum ShapeId : int {
   SHAPE_J3D17PT = 8,   // NoCornerShape3<true>
   SHAPE_J3D27PT = 9,   // BoxShape<3,1>
   SHAPE_POISSON = 10,  // NoCornerShape3<false>
-  SHAPE_COUNT = 11,
+  SHAPE_J1D3PT = 11,   // StarShape<1,1>
+  SHAPE_COUNT = 12,
   SHAPE_GENERIC = -1
 };
 

@@ -405,6 +405,9 @@ __global__ void __launch_bounds__(NW * 32, MINB)
   using Cfg = Stream2DCfg<SH, T, C, NW, S, E>;
   constexpr int R = Cfg::R;
   constexpr int TR = T * R;
+  // the dataflow dependency scan visits strips +-2: enough only while a
+  // strip's loaded columns overlap at most its two neighbours on each side
+  static_assert(3 * Cfg::HX <= Cfg::LC, "dependency scan needs HX <= VW");
 
   extern __shared__ __align__(1024) unsigned char smem[];
   const int warp = threadIdx.x >> 5;

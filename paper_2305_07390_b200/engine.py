@@ -7,10 +7,15 @@ for invalid parameters with the reference's messages (engine/params.py:52-90,
 engine/sm.py:39-48, engine/device.py:43-52).
 
 The reference engines *simulate* the two EBISU schemes on the CPU with access
-accounting.  Here the scheme runs as real sm_100a kernels; the returned
-``ExecutionTrace`` carries the GPU's closed-form counters (HBM cells loaded
-and stored, grid-wide syncs, lanes computed, valid cell-steps, work units)
-and the RST on-chip split of ``engine/rst.py`` for the cost model.
+accounting.  Here the scheme runs as real sm_100a kernels.  The returned
+``ExecutionTrace`` carries the counters the reference engine would emit for
+the caller's ``TilingParams`` (``accounting.py``: exact closed forms of
+engine/sm.py and engine/device.py under the trace.py:1-17 conventions, so
+``trace_summary``, the planner and the reference's accounting tests read it
+unchanged), and in ``trace.gpu`` the facts of the run that actually
+happened: kernel family, fused depth, launches, device time and the GPU
+geometry's own counters (cells loaded/stored by TMA, lanes computed, work
+units, grid-wide barriers).
 """
 
 from __future__ import annotations
@@ -19,7 +24,7 @@ import json
 from dataclasses import dataclass, field
 from fractions import Fraction
 
-from . import _native
+from . import _native, accounting
 from .grid import Grid, sweep
 from .shapes import StencilShape
 
@@ -102,22 +107,13 @@ class TilingParams:
 # ---------------------------------------------------------------------------
 
 def rst_shared_per_cell(stencil: StencilShape, ipt: int = ITEMS_PER_THREAD) -> Fraction:
-    offs = stencil.offsets
-    if stencil.dims == 1:
-        return Fraction(2)
-    if stencil.dims == 2:
-        return Fraction(2) + Fraction(len({o[1] for o in offs if o[1] != 0}))
-    own = {(i, 0) for i in range(ipt)}
-    needed = {(o[1] + i, o[2]) for o in offs for i in range(ipt)}
-    return Fraction(2) + Fraction(len(needed - own), ipt)
+    """engine/rst.py:26-45."""
+    return accounting.rst_shared_per_cell(stencil.offsets, stencil.dims, ipt)
 
 
 def onchip_charges(stencil: StencilShape, rst: bool) -> tuple[Fraction, Fraction]:
-    total = Fraction(len(stencil.taps) + 1)
-    if not rst:
-        return total, Fraction(0)
-    shared = rst_shared_per_cell(stencil)
-    return shared, total - shared
+    """engine/rst.py:48-51."""
+    return accounting.onchip_charges(stencil.offsets, stencil.dims, rst)
 
 
 # ---------------------------------------------------------------------------
@@ -139,11 +135,26 @@ class ExecutionTrace:
     device_tiles: int = 0
     halo_transactions: int = 0
     wall_phases: list = field(default_factory=list)
-    # GPU facts (not in the reference trace)
+    # GPU facts (not in the reference trace): what ran and the kernel
+    # geometry's own counters (native ebisu_trace)
     kernel: str = ""
     t_used: int = 0
     elapsed_ms: float = 0.0
     kernel_launches: int = 0
+    gpu: dict = field(default_factory=dict)
+
+    PHASE_CAP = accounting.PHASE_CAP
+
+    def charge_compute(self, lanes: int, shared_pc: Fraction, register_pc: Fraction):
+        self.cells_computed += lanes
+        self.onchip_shared += shared_pc * lanes
+        self.onchip_register += register_pc * lanes
+
+    def phase(self, tag: str, cells: int):
+        if len(self.wall_phases) < self.PHASE_CAP:
+            self.wall_phases.append((tag, cells))
+        elif len(self.wall_phases) == self.PHASE_CAP:
+            self.wall_phases.append(("truncated", 1))
 
     def merge(self, other: "ExecutionTrace"):
         for f in ("gm_loads", "gm_stores", "gm_halo_loads", "gm_halo_stores", "onchip_shared",
@@ -167,12 +178,16 @@ class ExecutionTrace:
             "device_tiles": self.device_tiles,
             "halo_transactions": self.halo_transactions,
             "wall_phases": [[tag, n] for tag, n in self.wall_phases],
-            "gpu": {"kernel": self.kernel, "t_used": self.t_used,
-                    "elapsed_ms": self.elapsed_ms, "kernel_launches": self.kernel_launches},
+            "gpu": dict(self.gpu, kernel=self.kernel, t_used=self.t_used,
+                        elapsed_ms=self.elapsed_ms, kernel_launches=self.kernel_launches),
         }
 
     def to_json(self) -> str:
         return json.dumps(self.to_dict(), sort_keys=True, indent=2) + "\n"
+
+    def phases_csv(self) -> str:
+        lines = ["phase,cells"] + [f"{tag},{n}" for tag, n in self.wall_phases]
+        return "\n".join(lines) + "\n"
 
 
 @dataclass
@@ -230,31 +245,48 @@ def _check(grid: Grid, stencil: StencilShape, params: TilingParams, scheme: str,
     params.validate(stencil, grid.extents)
 
 
+def _reference_trace(stencil: StencilShape, extents, params: TilingParams,
+                     steps: int) -> ExecutionTrace:
+    """Counters the reference engine emits for ``params`` (one epoch of
+    ``params.t`` steps, accounting.py); ``steps`` beyond one epoch add one
+    epoch's counters per further ``params.t`` steps (a shorter last epoch is
+    counted at its own depth)."""
+    import dataclasses
+
+    trace = ExecutionTrace()
+    offs = [tuple(o) for o in stencil.offsets]
+    done = 0
+    while done < steps:
+        depth = min(params.t, steps - done)
+        p = params if depth == params.t else dataclasses.replace(params, t=depth)
+        c = accounting.reference_counters(offs, stencil.dims, extents, p)
+        for f in ("gm_loads", "gm_stores", "gm_halo_loads", "gm_halo_stores", "onchip_shared",
+                  "onchip_register", "syncs_block", "syncs_device", "cells_computed",
+                  "cells_valid", "device_tiles", "halo_transactions"):
+            setattr(trace, f, getattr(trace, f) + getattr(c, f))
+        for tag, n in c.wall_phases:
+            if tag != "truncated":
+                trace.phase(tag, n)
+            elif len(trace.wall_phases) == trace.PHASE_CAP:
+                trace.phase(tag, n)
+        done += depth
+    return trace
+
+
 def _run(grid, stencil, params, scheme_code, steps=None, exact=True):
     steps = params.t if steps is None else steps
     out, tr = sweep(grid, stencil, steps, t=params.t, scheme=scheme_code, exact=exact,
                     trace=True, exc_param=ParamError)
-    trace = ExecutionTrace()
+    trace = _reference_trace(stencil, grid.extents, params, steps)
     if tr is not None:
-        trace.gm_loads = tr["gm_loads"]
-        trace.gm_stores = tr["gm_stores"]
-        trace.gm_halo_loads = tr["gm_halo_loads"]
-        trace.gm_halo_stores = tr["gm_halo_stores"]
-        trace.syncs_block = tr["syncs_block"]
-        trace.syncs_device = tr["syncs_device"]
-        trace.cells_computed = tr["cells_computed"]
-        trace.cells_valid = tr["cells_valid"]
-        trace.device_tiles = tr["device_tiles"]
         trace.kernel = tr["kernel"]
         trace.t_used = tr["t_used"]
         trace.elapsed_ms = tr["elapsed_ms"]
         trace.kernel_launches = tr["kernel_launches"]
-        sh, rg = onchip_charges(stencil, params.rst)
-        trace.onchip_shared = sh * trace.cells_computed
-        trace.onchip_register = rg * trace.cells_computed
-        load_tag = "prefetch-load" if params.prefetch else "load"
-        trace.wall_phases = [(load_tag, trace.gm_loads), ("compute", trace.cells_computed),
-                             ("store", trace.gm_stores)]
+        trace.gpu = {k: tr[k] for k in ("gm_loads", "gm_stores", "gm_halo_loads",
+                                        "gm_halo_stores", "syncs_block", "syncs_device",
+                                        "cells_computed", "cells_valid", "device_tiles",
+                                        "grid_ctas", "warps_per_cta")}
     return out, trace
 
 

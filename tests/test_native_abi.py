@@ -86,3 +86,15 @@ def test_run_without_device_fails_loudly():
     rc = lib.ebisu_run_host(ctypes.byref(st.c), 2, _native.extents_c((8, 8)), a.ctypes.data,
                             b.ctypes.data, 3, ctypes.byref(prm), None)
     assert rc == _native.EBISU_ERR_NO_DEVICE
+
+
+def test_integration_binding_is_the_tested_file():
+    """INTEGRATION.md §2 shows tools/stencilplan_b200_engine.py verbatim (the
+    file the GPU suite runs against the reference), with argtypes declared."""
+    doc = open(os.path.join(ROOT, "INTEGRATION.md")).read()
+    a = doc.index("<!-- BEGIN tools/stencilplan_b200_engine.py -->")
+    b = doc.index("<!-- END tools/stencilplan_b200_engine.py -->")
+    block = doc[a:b].split("```python\n", 1)[1].rsplit("```", 1)[0]
+    src = open(os.path.join(ROOT, "tools", "stencilplan_b200_engine.py")).read()
+    assert block == src
+    assert "_lib.ebisu_run_host.argtypes" in src
