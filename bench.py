@@ -135,6 +135,77 @@ def cpu_oracle_sample(seconds_target: float = 12.0, threads: int = 1) -> dict:
                       f"reference_run{'_threaded' if threads > 1 else ''} in {dt:.1f} s"}
 
 
+def lib_sha16() -> str:
+    import hashlib
+
+    from paper_2305_07390_b200 import _native
+
+    h = hashlib.sha256()
+    with open(_native.LIB_PATH, "rb") as f:
+        for chunk in iter(lambda: f.read(1 << 20), b""):
+            h.update(chunk)
+    return h.hexdigest()[:16]
+
+
+def measure_dram_traffic(tsteps: int, t: int, timeout: int = 300):
+    """DRAM bytes (read + write) of ONE launch of the headline kernel, measured
+    in this run: ncu (metrics only, one k_stream2d launch of the same sweep,
+    tools/prof_run.py) in a subprocess after the timed region.  Returns
+    (bytes or None, provenance dict).  A byte count, not a timing: nothing
+    timed here runs under the profiler."""
+    src = {"tool": "ncu --metrics dram__bytes_read.sum,dram__bytes_write.sum "
+                   "(in-run subprocess, one k_stream2d launch)",
+           "workload": f"{STENCIL} {N0}x{N1}, {tsteps} steps, t={t}"}
+    try:
+        src["lib_sha16"] = lib_sha16()
+        cmd = ["ncu", "--metrics", "dram__bytes_read.sum,dram__bytes_write.sum",
+               "--print-units", "base", "--clock-control", "none", "-k", "regex:k_stream2d",
+               "-c", "1", "--csv", sys.executable, os.path.join(ROOT, "tools", "prof_run.py"),
+               STENCIL, str(N0), str(tsteps), str(t)]
+        r = subprocess.run(cmd, capture_output=True, text=True, timeout=timeout, cwd=ROOT)
+        import csv
+        import io
+
+        rows = list(csv.reader(io.StringIO(r.stdout)))
+        start = next(i for i, row in enumerate(rows) if "Metric Name" in row)
+        rows = rows[start:]
+        hdr = rows[0]
+        name_i, val_i = hdr.index("Metric Name"), hdr.index("Metric Value")
+        unit_i = hdr.index("Metric Unit")
+        scale = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "Tbyte": 1e12}
+        tot = 0.0
+        seen = set()
+        for row in rows[1:]:
+            if row[name_i] in ("dram__bytes_read.sum", "dram__bytes_write.sum"):
+                tot += float(row[val_i].replace(",", "")) * scale.get(row[unit_i], 1)
+                seen.add(row[name_i])
+        if len(seen) != 2:
+            raise RuntimeError(f"metrics missing (rc {r.returncode}): {r.stderr[-200:]}")
+        return tot, src
+    except Exception as exc:  # ncu absent / no permission: report, do not guess
+        src["error"] = repr(exc)[:300]
+        return None, src
+
+
+# the paper's PTB bound THR = B_sc / (a_sm * S) (PAPER.md:65-84), a_sm = the
+# catalog's per-cell shared accesses with RST (StencilShape.sm_accesses_with_rst,
+# shapes.py:128-140), B_sc = 128 B/clk/SM of shared memory
+SMEM_B_PER_CLK_PER_SM = 128
+
+
+def ptb_fraction(stencil: str, gcells: float, sm_mhz, sms: int = 148, elem: int = 8) -> dict:
+    """Measured GCells/s vs the paper's PTB bound B_smem / (a_sm * S)
+    (SURVEY.md §8d), B_smem = SMs x 128 B/clk x the SM clock under load."""
+    from paper_2305_07390_b200.shapes import get_shape
+
+    mhz = float(sm_mhz) if sm_mhz else 1965.0
+    b_smem = sms * SMEM_B_PER_CLK_PER_SM * mhz * 1e6
+    a_sm = float(get_shape(stencil).sm_accesses_with_rst)
+    bound = b_smem / (a_sm * elem) / 1e9
+    return {"bound_gcells": round(bound, 1), "frac": round(gcells / bound, 3),
+            "a_sm": a_sm, "b_smem_gbs": round(b_smem / 1e9, 1), "sm_mhz": mhz}
+
+
 def dist_env():
     rank = int(os.environ.get("RANK", "0"))
     world = int(os.environ.get("WORLD_SIZE", "1"))
@@ -225,7 +296,8 @@ def extra_configs(eb, device, _native, torch, stream, hbm_peak):
              "kernel_launches": tr["kernel_launches"], "exact": True,
              "naive_roofline_frac": round(16 * g / hbm_peak, 3),
              "fp64_pipe_ceiling_gcells": round(_dp_ceiling_gcells(len(st.taps), sms, mhz), 1),
-             "valid_fraction": round(tr["cells_valid"] / max(1, tr["cells_computed"]), 3)}
+             "valid_fraction": round(tr["cells_valid"] / max(1, tr["cells_computed"]), 3),
+             "ptb": ptb_fraction(st.name, g, mhz, sms, 4 if extra.get("dtype") == "f32" else 8)}
         r.update(extra)
         out[name] = r
 
@@ -313,7 +385,9 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-3d", action="store_true", help="skip the config-4 3-D measurement")
-    ap.add_argument("--sweep-t", action="store_true", help="also time t=1..16 (config 2 sweep)")
+    ap.add_argument("--no-sweep", action="store_true", help="skip the config-2 t=1..16 sweep")
+    ap.add_argument("--no-traffic", action="store_true",
+                    help="skip the in-run ncu DRAM-traffic measurement")
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3
@@ -404,13 +478,9 @@ def main():
     # (persistent cooperative launch, grid.sync between epochs)
     launch_ms = statistics.mean(step_ms)
     achieved = ALG_BYTES_PER_CELL_STEP * cells_per_step / world / (launch_ms / 1e3) / 1e9
-    traffic = None
-    tf = os.path.join(ROOT, "profiles", "dram_traffic.json")
-    if os.path.exists(tf) and args.tsteps == TSTEPS and world == 1:
-        try:
-            traffic = json.load(open(tf)).get(f"{STENCIL}_t{args.t}")
-        except Exception:
-            traffic = None
+    traffic, traffic_src = None, None
+    if world == 1 and not args.no_traffic:
+        traffic, traffic_src = measure_dram_traffic(args.tsteps, args.t)
 
     line = {
         "metric": "GCells/s (fp64)", "value": value, "unit": "GCells/s", "n_gpus": world,
@@ -426,8 +496,12 @@ def main():
         "roofline": {"bound": "hbm", "kernel": "k_stream2d (stream2d_tb)",
                      "achieved": achieved, "peak": hbm_peak, "unit": "GB/s",
                      "frac": achieved / hbm_peak, "traffic": traffic,
+                     "traffic_source": traffic_src,
                      "peak_source": f"{peak_kind} hbm_gbs (MEASURED_PEAKS.json)",
-                     "algorithmic_bytes": "16 B per interior cell-step (naive load+store)"},
+                     "algorithmic_bytes": "16 B per interior cell-step (naive load+store)",
+                     "algorithmic_bytes_per_launch": ALG_BYTES_PER_CELL_STEP * cells_per_step
+                     // world},
+        "ptb": ptb_fraction(STENCIL, value / world, clocks.get("sm_mhz")),
         "clocks": clocks,
         "gpu_launches": (launches_per_step * args.steps) if launches_per_step
         else (runner.kernel_launches - launches0 if world > 1 else None),
@@ -462,7 +536,7 @@ def main():
                        "h2d_bytes_per_step": N0 * N1 * 8, "d2h_bytes_per_step": N0 * N1 * 8,
                        "api": "ebisu_run_host (pinned host buffers)"}
 
-    if args.sweep_t and world == 1:
+    if not args.no_sweep and world == 1:
         sweep = {}
         for t in range(1, 17):
             device.sweep_device(d_in, st, 96, out=d_out, scratch=d_scr, t=t)

@@ -214,19 +214,21 @@ PFN_cuTensorMapEncodeTiled_v12000 get_encode() {
 }
 
 int encode_map(CUtensorMap* m, const void* base, int rank, const long long* dims_fast_first,
-               const int* box_fast_first, int elem) {
+               const int* box_fast_first, int elem, long long row_pitch) {
   auto enc = get_encode();
   if (!enc) return fail(EBISU_ERR_CUDA, "cuTensorMapEncodeTiled unavailable");
   cuuint64_t gdim[3], gstride[2];
   cuuint32_t box[3], estr[3];
-  long long pitch = elem;
+  // byte strides of dims 1.. : the innermost row pitch may exceed the extent
+  // (padded rows of an odd last extent; TMA needs 16-byte strides)
+  long long pitch = (long long)elem * row_pitch;
   for (int i = 0; i < rank; ++i) {
     gdim[i] = (cuuint64_t)dims_fast_first[i];
     box[i] = (cuuint32_t)box_fast_first[i];
     estr[i] = 1;
     if (i + 1 < rank) {
-      pitch *= dims_fast_first[i];
       gstride[i] = (cuuint64_t)pitch;
+      pitch *= dims_fast_first[i + 1];
     }
   }
   CUresult r = enc(m, elem == 4 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT32 : CU_TENSOR_MAP_DATA_TYPE_FLOAT64,
@@ -416,7 +418,7 @@ int run_tb2d_stage(const ProblemDesc& p, const TbKernel* k, int epochs, int firs
   const int VW = k->valid_x;
   const int LC = k->box0, HX = (LC - VW) / 2;
   int aligned = 0;
-  const int nstrips = stream2d_nstrips(n1, LC, VW, HX, R, k->C, &aligned);
+  const int nstrips = stream2d_nstrips(n1, LC, VW, HX, R, k->C, &aligned, 16 / p.elem);
   const int span = p.z_hi - p.z_lo;  // output rows of this call
   int nseg = 1, seg_len = span;
   plan_segments(span, nstrips, total_warps, 2 * T * R, std::max(16, 2 * T * R), &nseg, &seg_len);
@@ -444,6 +446,7 @@ int run_tb2d_stage(const ProblemDesc& p, const TbKernel* k, int epochs, int firs
   L.first_src = first_src;
   L.first_dst = first_dst;
   L.aligned = aligned;
+  L.pitch = (int)(p.pitch ? p.pitch : p.ext[1]);
   for (int i = 0; i < 3; ++i) L.buf[i] = bufs[i];
   L.maps = maps;
   L.coeffs = p.coeffs;
@@ -518,7 +521,7 @@ int run_tb2d_stage(const ProblemDesc& p, const TbKernel* k, int epochs, int firs
   ctr->grid = grid;
   ctr->nw = k->NW;
   ctr->t_used = std::max(ctr->t_used, T);
-  ctr->kid = KID_STREAM2D;
+  if (ctr->kid == KID_NONE) ctr->kid = KID_STREAM2D;  // the first (main) stage names the run
   return EBISU_OK;
 }
 
@@ -540,7 +543,7 @@ int run_halo2d_stage(const ProblemDesc& p, const TbKernel* k, int epochs, int fi
   int aligned = n1 >= 2 * LW ? 1 : 0;
   int nstrips;
   if (aligned) {
-    const int mid = n1 - LW - VW;
+    const int mid = strip_last_x0(n1, LW, 2) - VW;
     nstrips = 2 + (mid > 0 ? (mid + VW - 1) / VW : 0);
   } else {
     nstrips = (n1 + VW - 1) / VW;
@@ -565,6 +568,7 @@ int run_halo2d_stage(const ProblemDesc& p, const TbKernel* k, int epochs, int fi
   L.z_lo = p.z_lo;
   L.z_hi = p.z_hi;
   L.aligned = aligned;
+  L.pitch = (int)(p.pitch ? p.pitch : p.ext[1]);
   for (int i = 0; i < 3; ++i) L.buf[i] = bufs[i];
   L.maps = maps;
   L.coeffs = p.coeffs;
@@ -615,7 +619,7 @@ int run_halo2d_stage(const ProblemDesc& p, const TbKernel* k, int epochs, int fi
   ctr->grid = grid;
   ctr->nw = k->NW;
   ctr->t_used = std::max(ctr->t_used, T);
-  ctr->kid = KID_HALO2D;
+  if (ctr->kid == KID_NONE) ctr->kid = KID_HALO2D;
   return EBISU_OK;
 }
 
@@ -630,24 +634,31 @@ int run_tb3d_stage(const ProblemDesc& p, const TbKernel* k, int epochs, int firs
   EB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k->func, k->NW * 32,
                                                         (size_t)k->smem_bytes));
   if (per_sm < 1) return fail(EBISU_ERR_CUDA, "stream3d kernel cannot be resident (T=%d)", T);
-  const int max_ctas = per_sm * di.sms;
+  int max_ctas = per_sm * di.sms;
+  const int cl = k->cluster;  // CTAs per tile (2: cluster pair along axis 1)
+  if (cl > 1) {
+    int nclusters = 0;
+    EB_CUDA(k->max_clusters(&nclusters));
+    if (nclusters < 1) return fail(EBISU_ERR_CUDA, "cluster kernel cannot be resident (T=%d)", T);
+    max_ctas = nclusters * cl;
+  }
   // edge-aligned tiles when two fit along an axis (stream2d_strip geometry)
-  auto tiles_along = [](int n, int L, int V, int* aligned) {
+  auto tiles_along = [](int n, int L, int V, int* aligned, int AL) {
     if (n >= 2 * L) {
       *aligned = 1;
-      const int mid = n - L - V;
+      const int mid = strip_last_x0(n, L, AL) - V;
       return 2 + (mid > 0 ? (mid + V - 1) / V : 0);
     }
     *aligned = 0;
     return (n + V - 1) / V;
   };
   int aligned_x = 0, aligned_y = 0;
-  const int ntx = tiles_along(n2, k->box0, k->valid_x, &aligned_x);
-  const int nty = tiles_along(n1, k->box1, k->valid_y, &aligned_y);
+  const int ntx = tiles_along(n2, k->box0, k->valid_x, &aligned_x, 16 / p.elem);
+  const int nty = tiles_along(n1, k->box1 * cl, k->valid_y, &aligned_y, 1);
   const long long tiles = (long long)ntx * nty;
   const int span = p.z_hi - p.z_lo;  // output planes of this call
   int nseg = 1, seg_len = span;
-  plan_segments(span, tiles, max_ctas, 3 * T * R, std::max(8, 2 * T * R), &nseg, &seg_len);
+  plan_segments(span, tiles, max_ctas / cl, 3 * T * R, std::max(8, 2 * T * R), &nseg, &seg_len);
   // (never below 4x the per-unit warm-up, which short segments pay in full;
   // EBISU_SEG3D=uniform: the balanced uniform length, for A/B measurement)
   const char* seg_mode = getenv("EBISU_SEG3D");
@@ -655,18 +666,19 @@ int run_tb3d_stage(const ProblemDesc& p, const TbKernel* k, int epochs, int firs
   int min_len = std::max(std::max(8, 2 * T * R), 4 * (T * R + T * k->z));
   if (const char* v = getenv("EBISU_SEGMIN3D")) min_len = std::max(8, atoi(v));  // tuning
   const std::vector<int> seg_start =
-      guided_segments(p.z_lo, p.z_hi, tiles, max_ctas, seg_len,
+      guided_segments(p.z_lo, p.z_hi, tiles, max_ctas / cl, seg_len,
                       uniform ? std::max(seg_len, min_len) : min_len,
                       (uniform && seg_rows_req <= 0) ? std::max(seg_len, min_len) : seg_rows_req);
   nseg = (int)seg_start.size() - 1;
   const long long units = tiles * nseg;
-  int grid = (int)std::min<long long>(max_ctas, units);
-  if (grid < 1) grid = 1;
+  int grid = (int)std::min<long long>(max_ctas, units * cl);
+  if (grid < cl) grid = cl;
   const bool coop = coop_req && di.coop && epochs > 1;
   TbLaunch L{};
   L.n0 = n0;
   L.n1 = n1;
   L.n2 = n2;
+  L.pitch = (int)(p.pitch ? p.pitch : p.ext[2]);
   L.ntx = ntx;
   L.nty = nty;
   L.aligned_x = aligned_x;
@@ -714,16 +726,16 @@ int run_tb3d_stage(const ProblemDesc& p, const TbKernel* k, int epochs, int firs
     loads += (uint64_t)n;  // every advance loads one plane (TMA zero-fills past n0)
     adv += (uint64_t)n;
   }
-  const uint64_t tile_cells = (uint64_t)k->box0 * (uint64_t)k->box1;
+  const uint64_t tile_cells = (uint64_t)k->box0 * (uint64_t)k->box1 * (uint64_t)cl;
   ctr->gm_loads += (uint64_t)epochs * loads * tile_cells * (uint64_t)ntx * nty;
   ctr->gm_stores += (uint64_t)epochs * (uint64_t)span * n1 * n2;
   ctr->cells_computed += (uint64_t)epochs * adv * (uint64_t)T * tile_cells * (uint64_t)ntx * nty;
   ctr->device_tiles += (uint64_t)epochs * (uint64_t)units;
-  ctr->syncs_block += (uint64_t)epochs * adv * (uint64_t)ntx * nty;
+  ctr->syncs_block += (uint64_t)epochs * adv * (uint64_t)ntx * nty * (uint64_t)cl;
   ctr->grid = grid;
   ctr->nw = k->NW;
   ctr->t_used = std::max(ctr->t_used, T);
-  ctr->kid = KID_STREAM3D;
+  if (ctr->kid == KID_NONE) ctr->kid = KID_STREAM3D;
   return EBISU_OK;
 }
 
@@ -750,12 +762,19 @@ int run_device_impl(const ProblemDesc& p0, const void* d_in, void* d_out, void* 
   std::vector<Stage> stages;
   const int D = p.dims;
   const bool uni = uniform_coeffs(p) && !(prm && prm->per_tap_products);
-  // TMA needs 16-byte row strides (even last extent) and 16-byte aligned bases.
-  bool tb_ok = (D == 2 || D == 3) && p.shape_id != SHAPE_GENERIC &&
-               scheme != EBISU_SCHEME_NAIVE && ((p.ext[D - 1] * p.elem) % 16 == 0) &&
-               (reinterpret_cast<uintptr_t>(d_in) % 16 == 0) &&
-               (reinterpret_cast<uintptr_t>(d_out) % 16 == 0) &&
-               (!d_scr || reinterpret_cast<uintptr_t>(d_scr) % 16 == 0);
+  // TMA needs 16-byte row strides (last extent a multiple of 16 bytes) and
+  // 16-byte aligned bases.  Otherwise the TB kernels run on row-padded copies
+  // (pitch rounded up to 16 bytes; TMA maps keep the true extent, so the pad
+  // is never read): one strided copy in, one out -- two grid passes per sweep
+  // instead of falling back to one-launch-per-step.
+  const bool tb_shape = (D == 2 || D == 3) && p.shape_id != SHAPE_GENERIC &&
+                        scheme != EBISU_SCHEME_NAIVE;
+  const bool tma_direct = ((p.ext[D - 1] * p.elem) % 16 == 0) &&
+                          (reinterpret_cast<uintptr_t>(d_in) % 16 == 0) &&
+                          (reinterpret_cast<uintptr_t>(d_out) % 16 == 0) &&
+                          (!d_scr || reinterpret_cast<uintptr_t>(d_scr) % 16 == 0);
+  bool pitched = tb_shape && !tma_direct && !ranged && !(prm && prm->frame_ready);
+  bool tb_ok = tb_shape && (tma_direct || pitched);
   if (tb_ok) {
     int t = (prm && prm->t > 0) ? prm->t : default_depth(p.shape_id);
     // fp32 windows cost half the registers: the 2-D star runs deeper
@@ -784,18 +803,30 @@ int run_device_impl(const ProblemDesc& p0, const void* d_in, void* d_out, void* 
       const int kid = D == 3 ? KID_STREAM3D : (fam == 1 ? KID_HALO2D : KID_STREAM2D);
       if (full > 0) stages.push_back({kid, k, (int)full});
       while (rem > 0) {
-        const int t2 = best_depth_leq(p.shape_id, D, (int)rem, exact, uni, fam, p.elem);
+        // remainder epochs: the deepest kernel <= rem of this family, else of
+        // the overlapped family (identical results), else the naive kernel
+        int f2 = fam;
+        int t2 = best_depth_leq(p.shape_id, D, (int)rem, exact, uni, f2, p.elem);
+        if (t2 == 0 && fam != 0) {
+          f2 = 0;
+          t2 = best_depth_leq(p.shape_id, D, (int)rem, exact, uni, f2, p.elem);
+        }
         if (t2 == 0) {
           stages.push_back({KID_NAIVE, nullptr, (int)rem});
           break;
         }
         const long long e2 = rem / t2;
-        stages.push_back({kid, find_tb(p.shape_id, D, t2, exact, uni, fam, p.elem), (int)e2});
+        const int kid2 = D == 3 ? KID_STREAM3D : (f2 == 1 ? KID_HALO2D : KID_STREAM2D);
+        stages.push_back({kid2, find_tb(p.shape_id, D, t2, exact, uni, f2, p.elem), (int)e2});
         rem -= e2 * t2;
       }
     }
   }
+  // a padded sweep is all-TB (the naive kernel works on the caller's layout)
+  if (pitched)
+    for (auto& s : stages) tb_ok = tb_ok && s.kind != KID_NAIVE;
   if (!tb_ok) {
+    pitched = false;
     stages.clear();
     stages.push_back({KID_NAIVE, nullptr, (int)steps});
   }
@@ -810,11 +841,37 @@ int run_device_impl(const ProblemDesc& p0, const void* d_in, void* d_out, void* 
                 nwrites);
   void* scr = d_scr;
   bool own_scr = false;
-  if (nwrites > 1 && !scr) {
+  void* pad[3] = {nullptr, nullptr, nullptr};  // padded in / out / scratch
+  const long long Xn = p.ext[D - 1];
+  const long long rows = total / Xn;
+  if (pitched) {
+    const long long al = 16 / p.elem;
+    p.pitch = (Xn + al - 1) / al * al;
+    const size_t pbytes = (size_t)(rows * p.pitch) * (size_t)p.elem;
+    for (int b = 0; b < 3; ++b) {
+      if (b == BUF_SCR && nwrites <= 1) continue;
+      cudaError_t e = cudaMallocAsync(&pad[b], pbytes, st);
+      if (e != cudaSuccess) {
+        for (int j = 0; j < b; ++j)
+          if (pad[j]) cudaFreeAsync(pad[j], st);
+        return cuda_fail(e, "cudaMallocAsync(padded buffer)");
+      }
+    }
+    cudaError_t e = cudaMemcpy2DAsync(pad[BUF_IN], (size_t)(p.pitch * p.elem), d_in,
+                                      (size_t)(Xn * p.elem), (size_t)(Xn * p.elem), (size_t)rows,
+                                      cudaMemcpyDeviceToDevice, st);
+    if (e != cudaSuccess) {
+      for (void* q : pad)
+        if (q) cudaFreeAsync(q, st);
+      return cuda_fail(e, "padded input copy");
+    }
+  } else if (nwrites > 1 && !scr) {
     EB_CUDA(cudaMallocAsync(&scr, bytes, st));
     own_scr = true;
   }
   void* bufs[3] = {const_cast<void*>(d_in), d_out, scr};
+  if (pitched)
+    for (int b = 0; b < 3; ++b) bufs[b] = pad[b];
   CUtensorMap maps[3];
   // Shared-product kernels never store frame cells (their windows hold
   // products, not values); the frame is constant, so copy it once into both
@@ -827,9 +884,11 @@ int run_device_impl(const ProblemDesc& p0, const void* d_in, void* d_out, void* 
       // frame_ready vouches for the caller's buffers only: scratch the
       // library just allocated holds no frame yet
       if (prm && prm->frame_ready && !(b == BUF_SCR && own_scr)) continue;
-      cudaError_t e = launch_frame_copy(p, d_in, bufs[b], st, di.sms);
+      cudaError_t e = launch_frame_copy(p, bufs[BUF_IN], bufs[b], st, di.sms);
       if (e != cudaSuccess) {
         if (own_scr) cudaFreeAsync(scr, st);
+        for (void* q : pad)
+          if (q) cudaFreeAsync(q, st);
         return cuda_fail(e, "frame copy launch");
       }
       ctr->launches += 1;
@@ -871,7 +930,8 @@ int run_device_impl(const ProblemDesc& p0, const void* d_in, void* d_out, void* 
             memset(&maps[i], 0, sizeof(CUtensorMap));
             continue;
           }
-          result = encode_map(&maps[i], bufs[i], D, dims_ff, box, p.elem);
+          result = encode_map(&maps[i], bufs[i], D, dims_ff, box, p.elem,
+                              p.pitch ? p.pitch : p.ext[D - 1]);
         }
         if (result) break;
       }
@@ -890,6 +950,16 @@ int run_device_impl(const ProblemDesc& p0, const void* d_in, void* d_out, void* 
     w += s.epochs;
   }
   if (own_scr) cudaFreeAsync(scr, st);
+  if (pitched) {
+    if (!result) {
+      cudaError_t e = cudaMemcpy2DAsync(d_out, (size_t)(Xn * p.elem), pad[BUF_OUT],
+                                        (size_t)(p.pitch * p.elem), (size_t)(Xn * p.elem),
+                                        (size_t)rows, cudaMemcpyDeviceToDevice, st);
+      if (e != cudaSuccess) result = cuda_fail(e, "padded output copy");
+    }
+    for (void* q : pad)
+      if (q) cudaFreeAsync(q, st);
+  }
   return result;
 }
 

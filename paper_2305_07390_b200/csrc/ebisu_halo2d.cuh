@@ -77,6 +77,7 @@ struct Halo2DArgs {
   int epochs;
   int first_src, first_dst;
   int aligned;  // edge-aligned strips (n1 >= 2*LW)
+  int pitch;    // row pitch of every buffer (elements, >= n1)
   double* buf[3];
   int* work;
 };
@@ -86,7 +87,7 @@ template <class SH, int T, int C, int NW, int S, bool EXACT, bool UNI, bool EDGE
 __device__ __forceinline__ int halo2d_unit(const CUtensorMap* tm, double* __restrict__ out,
                                            double* ring, uint64_t* bars, double* xh,
                                            uint64_t* advbar, uint32_t ring_cnt, uint32_t& adv,
-                                           int warp, int lane, int n0, int n1, int X0, int vlo,
+                                           int warp, int lane, int n0, int n1, int pitch, int X0, int vlo,
                                            int vhi, int r0, int r1, const Coefs<SH::NT>& cf) {
   using Cfg = Halo2DCfg<SH, T, C, NW, S>;
   constexpr int R = Cfg::R, Z = Cfg::Z, W = Cfg::W, NB = Cfg::NB, LC = Cfg::LC;
@@ -270,7 +271,7 @@ __device__ __forceinline__ int halo2d_unit(const CUtensorMap* tm, double* __rest
           bool qok = (q >= r0) && (q < r1);
           if (UNI && FROWS) qok = qok && !frow;
           if (qok) {
-            double* orow = out + (size_t)q * (size_t)n1 + (XW + lane * C);
+            double* orow = out + (size_t)q * (size_t)pitch + (XW + lane * C);
 #pragma unroll
             for (int c = 0; c < C; ++c)
               if ((stmask >> c) & 1u) orow[c] = nv[c];
@@ -344,18 +345,18 @@ __global__ void __launch_bounds__(NW * 32, MINB)
       const int strip = u % a.nstrips;
       const int seg = u / a.nstrips;
       const StripGeom g =
-          stream2d_strip(strip, a.nstrips, a.aligned, n1, Cfg::LW, Cfg::VW, Cfg::HX);
+          stream2d_strip(strip, a.nstrips, a.aligned, n1, Cfg::LW, Cfg::VW, Cfg::HX, 2);
       const int r0 = a.z_lo + seg * a.seg_len;
       const int r1 = min(a.z_hi, r0 + a.seg_len);
       const bool edge = (g.X0 < Cfg::R) || (g.X0 + Cfg::LW > n1 - Cfg::R);
       int used;
       if (edge)
         used = halo2d_unit<SH, T, C, NW, S, EXACT, UNI, true, SHIFT>(
-            tm, out, ring, bars, xh, advbar, ring_cnt, adv, warp, lane, n0, n1, g.X0, g.vlo,
+            tm, out, ring, bars, xh, advbar, ring_cnt, adv, warp, lane, n0, n1, a.pitch, g.X0, g.vlo,
             g.vhi, r0, r1, cf);
       else
         used = halo2d_unit<SH, T, C, NW, S, EXACT, UNI, false, SHIFT>(
-            tm, out, ring, bars, xh, advbar, ring_cnt, adv, warp, lane, n0, n1, g.X0, g.vlo,
+            tm, out, ring, bars, xh, advbar, ring_cnt, adv, warp, lane, n0, n1, a.pitch, g.X0, g.vlo,
             g.vhi, r0, r1, cf);
       ring_cnt += (uint32_t)used;
       __syncthreads();  // s_unit reuse; all warps done with the unit

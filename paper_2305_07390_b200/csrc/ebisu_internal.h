@@ -28,12 +28,13 @@ struct ProblemDesc {
   int shape_id;          // ShapeId or SHAPE_GENERIC
   int z_lo = 0, z_hi = 0;  // output planes [z_lo, z_hi) along axis 0 (set by the driver)
   int elem = 8;            // element bytes: 8 (fp64) or 4 (fp32)
+  long long pitch = 0;     // row pitch of the kernel buffers (elements; 0 = last extent)
 };
 
 cudaError_t launch_naive_step(const ProblemDesc& p, const void* in, void* out, bool exact,
                               cudaStream_t st, int num_sms);  // writes planes [z_lo, z_hi)
 cudaError_t launch_frame_copy(const ProblemDesc& p, const void* in, void* out,
-                              cudaStream_t st, int num_sms);
+                              cudaStream_t st, int num_sms);  // both buffers at p.pitch
 cudaError_t launch_splitmix(unsigned long long seed, long long start, long long n, double* out,
                             cudaStream_t st, int num_sms);
 cudaError_t launch_compare(const double* a, const double* b, long long n, long long* mism,
@@ -47,6 +48,7 @@ struct TbLaunch {
   int nstrips, nseg, seg_len;  // 2-D decomposition
   int z_lo, z_hi;              // output rows/planes [z_lo, z_hi) along axis 0
   int aligned;                 // 2-D: edge-aligned strips
+  int pitch;                   // row pitch of every buffer (elements; n_last or padded)
   int ntx, nty;                // 3-D decomposition (tiles along axis 2 / axis 1)
   int aligned_x, aligned_y;    // 3-D: edge-aligned tiles along axis 2 / axis 1
   const int* seg_start;        // 3-D: nseg+1 segment bounds along axis 0 (guided)
@@ -82,6 +84,8 @@ struct TbKernel {
   cudaError_t (*launch)(const TbLaunch&);
   int family;            // 0: overlapped (sm-tiling), 1: halo exchange (device-tiling)
   int elem;              // element bytes: 8 (fp64) or 4 (fp32)
+  int cluster = 1;       // CTAs per cluster along axis 1 (2: one tile over two SMs, DSMEM seam)
+  cudaError_t (*max_clusters)(int*) = nullptr;  // resident clusters (cluster kernels)
 };
 
 // All instantiated temporal-blocking kernels (ebisu_registry.cu).

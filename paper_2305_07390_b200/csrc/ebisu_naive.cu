@@ -197,15 +197,16 @@ cudaError_t launch_naive_step(const ProblemDesc& p, const void* in, void* out,
 template <class E>
 __global__ void __launch_bounds__(256) k_frame_copy(const E* __restrict__ in,
                                                     E* __restrict__ out, long long P,
-                                                    long long Y, long long X, int R0, int R1,
-                                                    int R2, long long row_lo, long long row_hi) {
+                                                    long long Y, long long X, long long pitch,
+                                                    int R0, int R1, int R2, long long row_lo,
+                                                    long long row_hi) {
   const int lane = threadIdx.x & 31;
   const long long warps = (long long)gridDim.x * (blockDim.x >> 5);
   for (long long row = row_lo + (long long)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
        row < row_hi; row += warps) {
     const long long pp = row / Y, y = row % Y;
-    const E* src = in + row * X;
-    E* dst = out + row * X;
+    const E* src = in + row * pitch;
+    E* dst = out + row * pitch;
     if (pp < R0 || pp >= P - R0 || y < R1 || y >= Y - R1) {
       for (long long j = lane; j < X; j += 32) dst[j] = src[j];
     } else {
@@ -237,18 +238,19 @@ cudaError_t launch_frame_copy(const ProblemDesc& p, const void* in, void* out,
   long long row_lo = (long long)p.z_lo * per, row_hi = z_hi * per;
   if (p.dims == 1) row_lo = 0, row_hi = 1;
   const long long rows = row_hi - row_lo;
+  const long long pitch = p.pitch ? p.pitch : X;
   long long blocks = (rows + 7) / 8;
   const long long cap = (long long)num_sms * 8;
   if (blocks > cap) blocks = cap;
   if (blocks < 1) blocks = 1;
   if (p.elem == 4)
     k_frame_copy<float><<<(unsigned)blocks, 256, 0, st>>>(
-        static_cast<const float*>(in), static_cast<float*>(out), P, Y, X, R0, R1, p.rad, row_lo,
-        row_hi);
+        static_cast<const float*>(in), static_cast<float*>(out), P, Y, X, pitch, R0, R1, p.rad,
+        row_lo, row_hi);
   else
     k_frame_copy<double><<<(unsigned)blocks, 256, 0, st>>>(
-        static_cast<const double*>(in), static_cast<double*>(out), P, Y, X, R0, R1, p.rad, row_lo,
-        row_hi);
+        static_cast<const double*>(in), static_cast<double*>(out), P, Y, X, pitch, R0, R1, p.rad,
+        row_lo, row_hi);
   return cudaGetLastError();
 }
 

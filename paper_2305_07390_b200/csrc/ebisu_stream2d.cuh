@@ -60,6 +60,7 @@ struct Stream2DArgs {
   int first_src;     // BufId of epoch 0's source
   int first_dst;     // BufId of epoch 0's destination
   int aligned;       // 1: edge-aligned strips (n1 >= 2*LC); 0: generic strips
+  int pitch;         // row pitch of every buffer (elements, >= n1; > n1 = padded rows)
   void* buf[3];      // device pointers by BufId (element type E of the kernel)
   long long* unit_clock;  // optional profiling: [units][2] start/end globaltimer (ns)
   int* work;         // per-epoch unit counters (dynamic scheduling), zeroed by the host
@@ -94,18 +95,29 @@ struct Stream2DCfg {
 // Strip geometry shared by host and device.  Aligned mode (n1 >= 2*LC):
 //   strip 0      X0 = 0,          valid [0, VW+HX)
 //   strip j      X0 = j*VW,       valid [j*VW+HX, (j+1)*VW+HX) clipped at xl
-//   last strip   X0 = n1-LC,      valid [xl, n1),  xl = n1-LC+HX
+//   last strip   X0 = xlast,      valid [xl, n1),  xl = xlast+HX
+//                (xlast = n1-LC rounded up to the TMA alignment)
 // Generic mode: X0 = j*VW-HX, valid [j*VW, (j+1)*VW) clipped at n1.
 struct StripGeom {
   int X0, vlo, vhi;
   int fc;  // frame columns: 0 none, 1 lane-0 left, 2 lane-31 right, 3 generic
 };
 
+// Start of the last strip in aligned mode: n1 - LC rounded UP to the TMA
+// alignment AL (elements per 16 bytes; 1 for axes other than the innermost).
+// With an even last extent that is n1 - LC exactly; with a padded odd extent
+// the last strip overhangs the domain by < AL columns (TMA zero-fills them;
+// they feed no stored cell: frame columns only carry their value).
+__host__ __device__ inline int strip_last_x0(int n1, int LC, int AL) {
+  return (n1 - LC + AL - 1) / AL * AL;
+}
+
 __host__ __device__ inline int stream2d_nstrips(int n1, int LC, int VW, int HX, int R, int C,
-                                                int* aligned) {
+                                                int* aligned, int AL = 1) {
   if (n1 >= 2 * LC && R <= C) {
     *aligned = 1;
-    const int mid = n1 - LC - VW;  // columns [VW+HX, n1-LC+HX) for middle strips
+    // columns [VW+HX, xlast+HX) for middle strips
+    const int mid = strip_last_x0(n1, LC, AL) - VW;
     return 2 + (mid > 0 ? (mid + VW - 1) / VW : 0);
   }
   *aligned = 0;
@@ -113,15 +125,17 @@ __host__ __device__ inline int stream2d_nstrips(int n1, int LC, int VW, int HX, 
 }
 
 __host__ __device__ inline StripGeom stream2d_strip(int j, int nstrips, int aligned, int n1,
-                                                    int LC, int VW, int HX) {
+                                                    int LC, int VW, int HX, int AL = 1) {
   StripGeom g;
   if (aligned) {
-    const int xl = n1 - LC + HX;
+    const int xlast = strip_last_x0(n1, LC, AL);
+    const int xl = xlast + HX;
     if (j == nstrips - 1) {
-      g.X0 = n1 - LC;
+      g.X0 = xlast;
       g.vlo = xl;
       g.vhi = n1;
-      g.fc = 2;
+      // frame columns in lane 31's last R cells only when the strip ends at n1
+      g.fc = xlast == n1 - LC ? 2 : 3;
     } else {
       g.X0 = j * VW;
       g.vlo = j == 0 ? 0 : j * VW + HX;
@@ -155,7 +169,7 @@ __host__ __device__ constexpr int pmod(int a) {
 template <class SH, int T, int C, int S, bool EXACT, bool UNI, int FC, class E, int SHIFT = 0>
 __device__ __forceinline__ int stream2d_unit(const CUtensorMap* tm, E* __restrict__ out,
                                               E* ring, uint64_t* bars, uint32_t ring_cnt,
-                                              int lane, int n0, int n1, const StripGeom& g,
+                                              int lane, int n0, int n1, int pitch, const StripGeom& g,
                                               int r0, int r1, const Coefs<SH::NT, E>& cf) {
   constexpr int R = SH::R;
   constexpr int W = 2 * R + 1;
@@ -354,7 +368,7 @@ __device__ __forceinline__ int stream2d_unit(const CUtensorMap* tm, E* __restric
           put(std::integral_constant<int, s>{}, uu, nv);
         } else {
           if (q >= r0 && q < r1) {
-            E* orow = out + (size_t)q * (size_t)n1 + (X0 + lane * C);
+            E* orow = out + (size_t)q * (size_t)pitch + (X0 + lane * C);
 #pragma unroll
             for (int c = 0; c < C; ++c) {
               bool st = stcol[c];
@@ -441,7 +455,7 @@ __global__ void __launch_bounds__(NW * 32, MINB)
       const int strip = u % a.nstrips;
       const int seg = u / a.nstrips;
       const StripGeom g =
-          stream2d_strip(strip, a.nstrips, a.aligned, n1, Cfg::LC, Cfg::VW, Cfg::HX);
+          stream2d_strip(strip, a.nstrips, a.aligned, n1, Cfg::LC, Cfg::VW, Cfg::HX, Cfg::AL);
       const int r0 = a.seg_start[seg];
       const int r1 = a.seg_start[seg + 1];
       if (a.flags && e > 0) {
@@ -455,7 +469,7 @@ __global__ void __launch_bounds__(NW * 32, MINB)
           const int js = strip - 2 + d % 5;
           if (js < 0 || js >= a.nstrips) continue;
           const StripGeom gj =
-              stream2d_strip(js, a.nstrips, a.aligned, n1, Cfg::LC, Cfg::VW, Cfg::HX);
+              stream2d_strip(js, a.nstrips, a.aligned, n1, Cfg::LC, Cfg::VW, Cfg::HX, Cfg::AL);
           // RAW: js wrote what we read; WAR: js reads what we overwrite
           const bool raw = gj.vlo < g.X0 + Cfg::LC && gj.vhi > g.X0;
           const bool war = gj.X0 < g.vhi && gj.X0 + Cfg::LC > g.vlo;
@@ -471,23 +485,23 @@ __global__ void __launch_bounds__(NW * 32, MINB)
       int used;
       if constexpr (R > C) {
         used = stream2d_unit<SH, T, C, S, EXACT, UNI, 3, E, SHIFT>(tm, out, ring, bars, ring_cnt,
-                                                                   lane, n0, n1, g, r0, r1, cf);
+                                                                   lane, n0, n1, a.pitch, g, r0, r1, cf);
       } else switch (g.fc) {
         case 0:
           used = stream2d_unit<SH, T, C, S, EXACT, UNI, 0, E, SHIFT>(tm, out, ring, bars, ring_cnt,
-                                                                     lane, n0, n1, g, r0, r1, cf);
+                                                                     lane, n0, n1, a.pitch, g, r0, r1, cf);
           break;
         case 1:
           used = stream2d_unit<SH, T, C, S, EXACT, UNI, 1, E, SHIFT>(tm, out, ring, bars, ring_cnt,
-                                                                     lane, n0, n1, g, r0, r1, cf);
+                                                                     lane, n0, n1, a.pitch, g, r0, r1, cf);
           break;
         case 2:
           used = stream2d_unit<SH, T, C, S, EXACT, UNI, 2, E, SHIFT>(tm, out, ring, bars, ring_cnt,
-                                                                     lane, n0, n1, g, r0, r1, cf);
+                                                                     lane, n0, n1, a.pitch, g, r0, r1, cf);
           break;
         default:
           used = stream2d_unit<SH, T, C, S, EXACT, UNI, 3, E, SHIFT>(tm, out, ring, bars, ring_cnt,
-                                                                     lane, n0, n1, g, r0, r1, cf);
+                                                                     lane, n0, n1, a.pitch, g, r0, r1, cf);
           break;
       }
       ring_cnt += (uint32_t)used;

@@ -33,7 +33,8 @@
 namespace ebisu {
 
 struct Stream3DArgs {
-  int n0, n1, n2;   // extents; plane pitch n1*n2, row pitch n2
+  int n0, n1, n2;   // extents
+  int pitch;        // row pitch of every buffer (elements, >= n2); plane pitch n1*pitch
   int nty, ntx;     // tiles along axis 1 / axis 2
   int aligned_y, aligned_x;  // edge-aligned tiles along axis 1 / axis 2
   int nseg;         // z segments
@@ -128,7 +129,7 @@ template <class SH, int T, int CY, int CX, int NWY, int S, int FL, bool EXACT, b
 __device__ __forceinline__ int stream3d_unit(const CUtensorMap* tm, E* __restrict__ out,
                                              E* ring, E* halo, uint64_t* bars,
                                              uint32_t ring_cnt, int warp, int lane, int n0,
-                                             int n1, int n2, int X0, int Y0, int xlo, int xhi,
+                                             int n1, int n2, int rp, int X0, int Y0, int xlo, int xhi,
                                              int ylo, int yhi, int r0, int r1,
                                              const Coefs<SH::NT, E>& cf) {
   using Cfg = Stream3DCfg<SH, T, CY, CX, NWY, S, FL, E>;
@@ -204,8 +205,8 @@ __device__ __forceinline__ int stream3d_unit(const CUtensorMap* tm, E* __restric
   const int wbl = warp < NWY - 1 ? warp + 1 : warp;
 
   // output pointer of this thread's first cell in plane q = k - T*Z
-  const long long plane = (long long)n1 * (long long)n2;
-  E* obase = out + ((long long)(Y0 + ty0) * n2 + (X0 + tx0));
+  const long long plane = (long long)n1 * (long long)rp;
+  E* obase = out + ((long long)(Y0 + ty0) * rp + (X0 + tx0));
 
   auto block = [&](int kbase, auto fpl_tag) {
     constexpr bool FPL = decltype(fpl_tag)::value;  // a target plane may be a frame plane
@@ -363,7 +364,7 @@ __device__ __forceinline__ int stream3d_unit(const CUtensorMap* tm, E* __restric
             for (int cy = 0; cy < CY; ++cy)
 #pragma unroll
               for (int cx = 0; cx < CX; ++cx)
-                if ((stmask >> (cy * CX + cx)) & 1u) o[(long long)cy * n2 + cx] = nv[cy][cx];
+                if ((stmask >> (cy * CX + cx)) & 1u) o[(long long)cy * rp + cx] = nv[cy][cx];
           }
         }
       });
@@ -408,7 +409,7 @@ template <class SH, int T, int CY, int CX, int NWY, int S, int FL, bool EXACT, b
 __device__ __forceinline__ int stream3d_unit_ps(const CUtensorMap* tm, E* __restrict__ out,
                                                 E* ring, E* halo, uint64_t* bars,
                                                 uint32_t ring_cnt, int warp, int lane, int n0,
-                                                int n1, int n2, int X0, int Y0, int xlo,
+                                                int n1, int n2, int rp, int X0, int Y0, int xlo,
                                                 int xhi, int ylo, int yhi, int r0, int r1,
                                                 const Coefs<SH::NT, E>& cf) {
   using Cfg = Stream3DCfg<SH, T, CY, CX, NWY, S, FL, E>;
@@ -476,8 +477,8 @@ __device__ __forceinline__ int stream3d_unit_ps(const CUtensorMap* tm, E* __rest
   };
   const int wa = warp > 0 ? warp - 1 : warp;
   const int wbl = warp < NWY - 1 ? warp + 1 : warp;
-  const long long plane = (long long)n1 * (long long)n2;
-  E* obase = out + ((long long)(Y0 + ty0) * n2 + (X0 + tx0));
+  const long long plane = (long long)n1 * (long long)rp;
+  E* obase = out + ((long long)(Y0 + ty0) * rp + (X0 + tx0));
 
   auto advance = [&](int k, auto fpl_tag) {
     constexpr bool FPL = decltype(fpl_tag)::value;
@@ -580,7 +581,7 @@ __device__ __forceinline__ int stream3d_unit_ps(const CUtensorMap* tm, E* __rest
           for (int cy = 0; cy < CY; ++cy)
 #pragma unroll
             for (int cx = 0; cx < CX; ++cx)
-              if ((stmask >> (cy * CX + cx)) & 1u) o[(long long)cy * n2 + cx] = nv[cy][cx];
+              if ((stmask >> (cy * CX + cx)) & 1u) o[(long long)cy * rp + cx] = nv[cy][cx];
         }
       }
     });
@@ -626,7 +627,7 @@ template <class SH, int T, int CY, int CX, int NWY, int S, int FL, bool EXACT, b
 __device__ __forceinline__ int stream3d_unit_pm(const CUtensorMap* tm, E* __restrict__ out,
                                                 E* ring, E* halo, uint64_t* bars,
                                                 uint32_t ring_cnt, int warp, int lane, int n0,
-                                                int n1, int n2, int X0, int Y0, int xlo,
+                                                int n1, int n2, int rp, int X0, int Y0, int xlo,
                                                 int xhi, int ylo, int yhi, int r0, int r1,
                                                 const Coefs<SH::NT, E>& cf) {
   using Cfg = Stream3DCfg<SH, T, CY, CX, NWY, S, FL, E>;
@@ -693,8 +694,8 @@ __device__ __forceinline__ int stream3d_unit_pm(const CUtensorMap* tm, E* __rest
   };
   const int wa = warp > 0 ? warp - 1 : warp;
   const int wbl = warp < NWY - 1 ? warp + 1 : warp;
-  const long long plane = (long long)n1 * (long long)n2;
-  E* obase = out + ((long long)(Y0 + ty0) * n2 + (X0 + tx0));
+  const long long plane = (long long)n1 * (long long)rp;
+  E* obase = out + ((long long)(Y0 + ty0) * rp + (X0 + tx0));
 
   // sum of the taps with axis-0 offset DZ over the gathered neighbourhood,
   // starting from `acc` (FIRST: the run opens the target's sum)
@@ -804,7 +805,7 @@ __device__ __forceinline__ int stream3d_unit_pm(const CUtensorMap* tm, E* __rest
           for (int cy = 0; cy < CY; ++cy)
 #pragma unroll
             for (int cx = 0; cx < CX; ++cx)
-              if ((stmask >> (cy * CX + cx)) & 1u) o[(long long)cy * n2 + cx] = nv[cy][cx];
+              if ((stmask >> (cy * CX + cx)) & 1u) o[(long long)cy * rp + cx] = nv[cy][cx];
         }
       }
     });
@@ -878,7 +879,7 @@ __global__ void __launch_bounds__(NWY * 32, MINB)
       // edge-aligned tiles (a.aligned_x/y): the first tile starts at the
       // domain edge and the last ends there -- the frame needs no halo, so
       // those tiles keep the margin on one side only (fewer tiles per axis)
-      const StripGeom gx = stream2d_strip(tx, a.ntx, a.aligned_x, n2, Cfg::LX, Cfg::VX, Cfg::HX);
+      const StripGeom gx = stream2d_strip(tx, a.ntx, a.aligned_x, n2, Cfg::LX, Cfg::VX, Cfg::HX, Cfg::AL);
       const StripGeom gy = stream2d_strip(ty, a.nty, a.aligned_y, n1, Cfg::LY, Cfg::VY, Cfg::HY);
       const int X0 = gx.X0, Y0 = gy.X0;
       const int TR = T * R;
@@ -888,25 +889,25 @@ __global__ void __launch_bounds__(NWY * 32, MINB)
       if constexpr (pm_eligible<SH>() && (FL & 1) == 0) {
         if (edge)
           used = stream3d_unit_pm<SH, T, CY, CX, NWY, S, FL, EXACT, UNI, true, E>(
-              tm, out, ring, halo, bars, ring_cnt, warp, lane, n0, n1, n2, X0, Y0, gx.vlo, gx.vhi,
+              tm, out, ring, halo, bars, ring_cnt, warp, lane, n0, n1, n2, a.pitch, X0, Y0, gx.vlo, gx.vhi,
               gy.vlo, gy.vhi, r0, r1, cf);
         else
           used = stream3d_unit_pm<SH, T, CY, CX, NWY, S, FL, EXACT, UNI, false, E>(
-              tm, out, ring, halo, bars, ring_cnt, warp, lane, n0, n1, n2, X0, Y0, gx.vlo, gx.vhi,
+              tm, out, ring, halo, bars, ring_cnt, warp, lane, n0, n1, n2, a.pitch, X0, Y0, gx.vlo, gx.vhi,
               gy.vlo, gy.vhi, r0, r1, cf);
       } else if constexpr (ps_eligible<SH>() && (FL & 1) == 0) {
         if (edge)
           used = stream3d_unit_ps<SH, T, CY, CX, NWY, S, FL, EXACT, UNI, true, E>(
-              tm, out, ring, halo, bars, ring_cnt, warp, lane, n0, n1, n2, X0, Y0, gx.vlo, gx.vhi, gy.vlo, gy.vhi, r0, r1, cf);
+              tm, out, ring, halo, bars, ring_cnt, warp, lane, n0, n1, n2, a.pitch, X0, Y0, gx.vlo, gx.vhi, gy.vlo, gy.vhi, r0, r1, cf);
         else
           used = stream3d_unit_ps<SH, T, CY, CX, NWY, S, FL, EXACT, UNI, false, E>(
-              tm, out, ring, halo, bars, ring_cnt, warp, lane, n0, n1, n2, X0, Y0, gx.vlo, gx.vhi, gy.vlo, gy.vhi, r0, r1, cf);
+              tm, out, ring, halo, bars, ring_cnt, warp, lane, n0, n1, n2, a.pitch, X0, Y0, gx.vlo, gx.vhi, gy.vlo, gy.vhi, r0, r1, cf);
       } else if (edge)
         used = stream3d_unit<SH, T, CY, CX, NWY, S, FL, EXACT, UNI, true, E>(
-            tm, out, ring, halo, bars, ring_cnt, warp, lane, n0, n1, n2, X0, Y0, gx.vlo, gx.vhi, gy.vlo, gy.vhi, r0, r1, cf);
+            tm, out, ring, halo, bars, ring_cnt, warp, lane, n0, n1, n2, a.pitch, X0, Y0, gx.vlo, gx.vhi, gy.vlo, gy.vhi, r0, r1, cf);
       else
         used = stream3d_unit<SH, T, CY, CX, NWY, S, FL, EXACT, UNI, false, E>(
-            tm, out, ring, halo, bars, ring_cnt, warp, lane, n0, n1, n2, X0, Y0, gx.vlo, gx.vhi, gy.vlo, gy.vhi, r0, r1, cf);
+            tm, out, ring, halo, bars, ring_cnt, warp, lane, n0, n1, n2, a.pitch, X0, Y0, gx.vlo, gx.vhi, gy.vlo, gy.vhi, r0, r1, cf);
       ring_cnt += (uint32_t)used;
       __syncthreads();  // halo buffers and s_unit are reused by the next unit
     }

@@ -8,6 +8,7 @@
 #include "ebisu_stream2d.cuh"
 #include "ebisu_stream3d.cuh"
 #include "ebisu_halo2d.cuh"
+#include "ebisu_stream3d_cl.cuh"
 
 namespace ebisu {
 
@@ -33,6 +34,7 @@ cudaError_t launch_stream2d(const TbLaunch& L) {
   a.first_src = L.first_src;
   a.first_dst = L.first_dst;
   a.aligned = L.aligned;
+  a.pitch = L.pitch;
   if (L.nseg > EBISU_MAX_SEGS) return cudaErrorInvalidValue;
   for (int j = 0; j <= L.nseg; ++j) a.seg_start[j] = L.seg_start[j];
   for (int i = 0; i < 3; ++i) a.buf[i] = L.buf[i];
@@ -91,6 +93,7 @@ cudaError_t launch_stream3d(const TbLaunch& L) {
   a.n0 = L.n0;
   a.n1 = L.n1;
   a.n2 = L.n2;
+  a.pitch = L.pitch;
   a.nty = L.nty;
   a.ntx = L.ntx;
   a.aligned_x = L.aligned_x;
@@ -133,6 +136,90 @@ cudaError_t launch_stream3d(const TbLaunch& L) {
         (int)sizeof(E)                                                                        \
   }
 
+// 2-CTA cluster kernel (ebisu_stream3d_cl.cuh): cudaLaunchKernelEx with a
+// (2, 1, 1) cluster, cooperative when the sweep has several epochs.
+template <class SH, int T, int CY, int CX, int NWY, int S, bool UNI, int MINB>
+cudaError_t launch_stream3d_cl(const TbLaunch& L) {
+  using ClCfg = Stream3DClCfg<SH, T, CY, CX, NWY, S>;
+  auto kern = k_stream3d_cl<SH, T, CY, CX, NWY, S, UNI, MINB>;
+  cudaError_t err =
+      cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, ClCfg::SMEM_BYTES);
+  if (err != cudaSuccess) return err;
+  TmapSet maps;
+  memcpy(&maps.m[0], L.maps, 3 * sizeof(CUtensorMap));
+  Stream3DArgs a;
+  a.n0 = L.n0;
+  a.n1 = L.n1;
+  a.n2 = L.n2;
+  a.pitch = L.pitch;
+  a.nty = L.nty;
+  a.ntx = L.ntx;
+  a.aligned_x = L.aligned_x;
+  a.aligned_y = L.aligned_y;
+  a.nseg = L.nseg;
+  a.seg_len = L.seg_len;
+  a.z_lo = L.z_lo;
+  a.z_hi = L.z_hi;
+  if (L.nseg > EBISU_MAX_SEGS) return cudaErrorInvalidValue;
+  for (int j = 0; j <= L.nseg; ++j) a.seg_start[j] = L.seg_start[j];
+  a.epochs = L.epochs;
+  a.first_src = L.first_src;
+  a.first_dst = L.first_dst;
+  for (int i = 0; i < 3; ++i) a.buf[i] = L.buf[i];
+  a.work = L.work;
+  Coefs<SH::NT, double> cf;
+  for (int i = 0; i < SH::NT; ++i) cf.c[i] = L.coeffs[i];
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = dim3(L.grid);
+  cfg.blockDim = dim3(NWY * 32);
+  cfg.dynamicSmemBytes = (size_t)ClCfg::SMEM_BYTES;
+  cfg.stream = L.stream;
+  cudaLaunchAttribute attrs[2];
+  attrs[0].id = cudaLaunchAttributeClusterDimension;
+  attrs[0].val.clusterDim.x = 2;
+  attrs[0].val.clusterDim.y = 1;
+  attrs[0].val.clusterDim.z = 1;
+  attrs[1].id = cudaLaunchAttributeCooperative;
+  attrs[1].val.cooperative = L.cooperative ? 1 : 0;
+  cfg.attrs = attrs;
+  cfg.numAttrs = 2;
+  return cudaLaunchKernelEx(&cfg, kern, maps, a, cf);
+}
+
+// resident clusters of the cluster kernel (occupancy query for the planner)
+template <class SH, int T, int CY, int CX, int NWY, int S, bool UNI, int MINB>
+cudaError_t clusters_stream3d_cl(int* n) {
+  using ClCfg = Stream3DClCfg<SH, T, CY, CX, NWY, S>;
+  auto kern = k_stream3d_cl<SH, T, CY, CX, NWY, S, UNI, MINB>;
+  cudaError_t err =
+      cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, ClCfg::SMEM_BYTES);
+  if (err != cudaSuccess) return err;
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = dim3(2);
+  cfg.blockDim = dim3(NWY * 32);
+  cfg.dynamicSmemBytes = (size_t)ClCfg::SMEM_BYTES;
+  cudaLaunchAttribute attr;
+  attr.id = cudaLaunchAttributeClusterDimension;
+  attr.val.clusterDim.x = 2;
+  attr.val.clusterDim.y = 1;
+  attr.val.clusterDim.z = 1;
+  cfg.attrs = &attr;
+  cfg.numAttrs = 1;
+  return cudaOccupancyMaxActiveClusters(n, (const void*)kern, &cfg);
+}
+
+#define EBISU_S3D_CL_ENTRY(SHAPE_ID, SH, T, CY, CX, NWY, S, UNI, MINB)                        \
+  TbKernel {                                                                                  \
+    SHAPE_ID, 3, T, CX, NWY, S, 1, UNI, Stream3DClCfg<SH, T, CY, CX, NWY, S>::SMEM_BYTES,     \
+        Stream3DCfg<SH, T, CY, CX, NWY, S, 0, double>::LX,                                    \
+        Stream3DCfg<SH, T, CY, CX, NWY, S, 0, double>::LY, 1,                                 \
+        Stream3DCfg<SH, T, CY, CX, NWY, S, 0, double>::VX,                                    \
+        Stream3DClCfg<SH, T, CY, CX, NWY, S>::VY2, 1, 2,                                      \
+        (const void*)&k_stream3d_cl<SH, T, CY, CX, NWY, S, (UNI) != 0, MINB>,                 \
+        &launch_stream3d_cl<SH, T, CY, CX, NWY, S, (UNI) != 0, MINB>, 0, 8, 2,                \
+        &clusters_stream3d_cl<SH, T, CY, CX, NWY, S, (UNI) != 0, MINB>                        \
+  }
+
 template <class SH, int T, int C, int NW, int S, bool EXACT, bool UNI, int MINB,
           int SHIFT = 0>
 cudaError_t launch_halo2d(const TbLaunch& L) {
@@ -155,6 +242,7 @@ cudaError_t launch_halo2d(const TbLaunch& L) {
   a.first_src = L.first_src;
   a.first_dst = L.first_dst;
   a.aligned = L.aligned;
+  a.pitch = L.pitch;
   for (int i = 0; i < 3; ++i) a.buf[i] = static_cast<double*>(L.buf[i]);
   a.work = L.work;
   Coefs<SH::NT> cf;

@@ -35,6 +35,10 @@ S3D = [
     ("SHAPE_J3D7PT", "StarShape<3, 1>", "j3d7pt",
      [(1, 4, 2, 8, 4, 0, 1), (2, 4, 2, 8, 4, 0, 1), (3, 4, 2, 8, 4, 0, 1), (4, 4, 2, 8, 4, 0, 1),
       (2, 2, 2, 16, 4, 0, 1), (3, 2, 2, 16, 4, 0, 1)]),
+# (taller one-CTA tiles measured and dropped: 9-13 warps get <= 168 registers
+# per thread (3 warps per SMSP) and spill -- t=4 x 10 warps 269, x 9 warps 321,
+# t=3 x 12 warps 482, x 13 warps 295 vs 681 / 701 for 8 warps; a taller tile
+# needs a second SM's registers: the 2-CTA cluster kernel)
     ("SHAPE_J3D13PT", "StarShape<3, 2>", "j3d13pt", [(1, 4, 2, 8, 4, 0, 1), (2, 4, 2, 8, 4, 0, 1)]),
     ("SHAPE_J3D27PT", "BoxShape<3, 1>", "j3d27pt",
      [(1, 4, 2, 8, 4, 0, 1), (2, 4, 2, 8, 4, 0, 1), (1, 2, 2, 16, 4, 0, 1), (2, 2, 2, 16, 4, 0, 1)]),
@@ -43,16 +47,26 @@ S3D = [
     ("SHAPE_POISSON", "NoCornerShape3<false>", "poisson", [(1, 4, 2, 8, 4, 0, 1), (2, 4, 2, 8, 4, 0, 1)]),
 ]
 
+# 2-CTA cluster kernels (ebisu_stream3d_cl.cuh: one 64x64 tile over two SMs,
+# DSMEM seam exchange), shared-product fp64: (T, CY, CX, NWY, S); registered
+# after the one-CTA kernels of the same depth (opt-in variants).  Measured
+# (512^3 x 500): t=3 601 / t=2 497 GCells/s vs 701 / 585 for one CTA despite
+# V 0.72 vs 0.65 -- the pair runs at the pace of its slower SM every advance;
+# t=4 does not fit the register file with the seam state (424 B spills, 372)
+CL3D = {"j3d7pt": [(3, 4, 2, 8, 4), (2, 4, 2, 8, 4)]}
+
 # fp32 (north-star 1e-5 mode), shared-product kernels only (uniform
 # coefficients; other stencils run the fp32 naive kernel).  Floats halve the
 # window registers, so 2-D strips are 32*8 = 256 columns wide (the TMA box
 # limit) at the same register cost as fp64 with 4 cells per lane.
-F32_2D = {"j2d5pt": [(4, 8), (8, 8), (12, 4), (16, 4)], "j2d9pt_gol": [(2, 8)],
-          "j2d9pt": [(2, 8)], "j2d25pt": [(2, 4)], "j2d13pt": [(2, 4)], "j2ds25pt": [(1, 4)]}
+# (depths 1 and 2 of every shape keep sweep remainders on the TB kernels)
+F32_2D = {"j2d5pt": [(4, 8), (8, 8), (12, 4), (16, 4), (1, 8), (2, 8)],
+          "j2d9pt_gol": [(2, 8), (1, 8)], "j2d9pt": [(2, 8), (1, 8)], "j2d25pt": [(2, 4), (1, 4)],
+          "j2d13pt": [(2, 4), (1, 4)], "j2ds25pt": [(1, 4)]}
 # fp32 3-D: half the registers -> 12-warp 48x64 tiles (t=4: 1284 vs 1151
 # GCells/s with 8 warps; t=5/6 and 4x4-cell tiles measured slower)
 F32_3D = {"j3d7pt": [(4, 4, 2, 12, 4, 0, 1), (3, 4, 2, 12, 4, 0, 1), (2, 4, 2, 8, 4, 0, 1),
-                     (4, 4, 2, 8, 4, 0, 1)],
+                     (4, 4, 2, 8, 4, 0, 1), (1, 4, 2, 8, 4, 0, 1)],
           "j3d27pt": [(1, 4, 2, 8, 4, 0, 1), (2, 4, 2, 8, 4, 0, 1)],
           "j3d13pt": [(1, 4, 2, 8, 4, 0, 1)], "j3d17pt": [(1, 4, 2, 8, 4, 0, 1)],
           "poisson": [(1, 4, 2, 8, 4, 0, 1)]}
@@ -111,8 +125,17 @@ def _write_tu(arr, fn, tag, sh, entries):
     lines.append("};\n")
     lines.append(f"const int {arr}_n = {len(entries)};\n")
     lines.append("}  // namespace ebisu\n")
-    with open(os.path.join(HERE, fn), "w") as f:
-        f.write("".join(lines))
+    _write_if_changed(os.path.join(HERE, fn), "".join(lines))
+
+
+def _write_if_changed(path, text):
+    """Keep the mtime of unchanged outputs (make then rebuilds only what changed)."""
+    if os.path.exists(path):
+        with open(path) as f:
+            if f.read() == text:
+                return
+    with open(path, "w") as f:
+        f.write(text)
 
 
 def main():
@@ -147,6 +170,9 @@ def main():
             entries = [f"    EBISU_S3D_ENTRY({sid}, SH_{tag}, {t}, {cy}, {cx}, {nwy}, {ss}, "
                        f"{dec}, {exact}, {uni}, {mb}, double),\n"
                        for t, cy, cx, nwy, ss, dec, mb in lst]
+            if kind == "u" and tag in CL3D:
+                entries += [f"    EBISU_S3D_CL_ENTRY({sid}, SH_{tag}, {t}, {cy}, {cx}, {nwy}, {ss}, "
+                            f"1, 1),\n" for t, cy, cx, nwy, ss in CL3D[tag]]
             _write_tu(arr, f"ebisu_inst_{tag}_{kind}.cu", tag, sh, entries)
             units.append(arr)
     for sid, sh, tag, _ in S2D:
@@ -190,11 +216,10 @@ def main():
         reg.append(f"    all.insert(all.end(), {arr}, {arr} + {arr}_n);\n")
     reg.append("  });\n  *count = (int)all.size();\n  return all.data();\n}\n")
     reg.append("}  // namespace ebisu\n")
-    with open(os.path.join(HERE, "ebisu_registry.cu"), "w") as f:
-        f.write("".join(reg))
-    with open(os.path.join(HERE, "instances.mk"), "w") as f:
-        f.write("# GENERATED by gen_instances.py\nINST_SRCS := "
-                + " ".join(f"ebisu_inst_{u[2:]}.cu" for u in units) + "\n")
+    _write_if_changed(os.path.join(HERE, "ebisu_registry.cu"), "".join(reg))
+    _write_if_changed(os.path.join(HERE, "instances.mk"),
+                      "# GENERATED by gen_instances.py\nINST_SRCS := "
+                      + " ".join(f"ebisu_inst_{u[2:]}.cu" for u in units) + "\n")
 
 
 if __name__ == "__main__":

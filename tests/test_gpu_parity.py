@@ -79,14 +79,32 @@ def test_2d_shapes_all_depths_ragged(name):
             assert np.array_equal(out.cells, ref), (name, t, (n0, n1), steps, tr)
 
 
-def test_odd_width_and_generic_shapes_use_naive_kernel():
-    # odd row pitch (TMA needs 16-byte strides) and non-catalog tap orders
+def test_odd_width_runs_padded_tb_and_generic_shapes_use_naive_kernel():
+    # odd row pitch (TMA needs 16-byte strides): the TB kernel runs on
+    # row-padded copies; every depth, both schemes, fp64 + fp32 layouts
     st = _shape("j2d5pt")
-    g = eb.random_grid((37, 131), 5)
-    out, tr = eb.sweep(g, st, 23, trace=True)
-    assert np.array_equal(out.cells, oracle_run(g.cells, taps_of(st), 23))
+    for ext, steps in (((37, 131), 23), ((200, 257), 50), ((64, 1023), 19)):
+        g = eb.random_grid(ext, 5)
+        ref = oracle_run(g.cells, taps_of(st), steps)
+        for t in (0, 1, 3, 8):
+            out, tr = eb.sweep(g, st, steps, t=t, trace=True)
+            assert tr["kernel"] == "stream2d_tb", (ext, t, tr)
+            assert np.array_equal(out.cells, ref), (ext, t)
+        out, tr = eb.sweep(g, st, steps, scheme=_native.SCHEME_DEVICE_TILING, trace=True)
+        assert tr["kernel"] == "halo2d_tb", tr
+        assert np.array_equal(out.cells, ref), ext
+        out, tr = eb.sweep(g, st, steps, trace=True, dtype=np.float32)
+        assert tr["kernel"] == "stream2d_tb", tr
+        assert np.max(np.abs(out.cells - ref)) <= 1e-5 * np.max(np.abs(ref)), ext
+    for name in ("j2d9pt", "j2d25pt", "j2ds25pt"):
+        st = _shape(name)
+        g = eb.random_grid((60, 2 * 128 + 3 * st.radius * 4 + 1), 3)
+        out, tr = eb.sweep(g, st, 5, trace=True)
+        assert tr["kernel"] == "stream2d_tb", (name, tr)
+        assert np.array_equal(out.cells, oracle_run(g.cells, taps_of(st), 5)), name
     # reversed tap order = a different summation order -> generic kernel, still exact
-    rev = eb.StencilShape("rev", 2, tuple(reversed(st.taps)), 10, 2, 6, 4.0)
+    rev = eb.StencilShape("rev", 2, tuple(reversed(st.taps)), 2 * len(st.taps), 2,
+                          len(st.taps) + 1, 4.0)
     g = eb.random_grid((40, 64), 9)
     out, tr = eb.sweep(g, rev, 7, trace=True)
     assert tr["kernel"] == "naive_step"
@@ -165,12 +183,14 @@ def test_3d_lane_variants_and_persistence():
             assert np.array_equal(out.cells, ref), (t, persistent)
 
 
-def test_3d_odd_last_extent_uses_naive():
-    st = _shape("j3d7pt")
-    g = eb.random_grid((17, 19, 23), 5)
-    out, tr = eb.sweep(g, st, 5, trace=True)
-    assert tr["kernel"] == "naive_step"
-    assert np.array_equal(out.cells, oracle_run(g.cells, taps_of(st), 5))
+def test_3d_odd_last_extent_runs_padded_tb():
+    for name in ("j3d7pt", "j3d27pt", "j3d13pt"):
+        st = _shape(name)
+        for ext in ((17, 19, 23), (20, 45, 71)):
+            g = eb.random_grid(ext, 5)
+            out, tr = eb.sweep(g, st, 5, trace=True)
+            assert tr["kernel"] == "stream3d_tb", (name, ext, tr)
+            assert np.array_equal(out.cells, oracle_run(g.cells, taps_of(st), 5)), (name, ext)
 
 
 def test_full_size_512_cubed_against_oracle():

@@ -10,7 +10,10 @@ st = eb.get_shape(name)
 d_in = device.random_grid_device((n,) * st.dims, seed=1)
 out = torch.empty_like(d_in); scr = torch.empty_like(d_in)
 scheme = int(sys.argv[6]) if len(sys.argv) > 6 else 0
-prm = _native.make_params(scheme=scheme, t=t, variant=var)
+# EBISU_PERSISTENT=0: one launch per epoch (ncu cannot replay a cooperative
+# cluster launch)
+prm = _native.make_params(scheme=scheme, t=t, variant=var,
+                          persistent=os.environ.get("EBISU_PERSISTENT", "1") != "0")
 for _ in range(2):
     _, tr = device.sweep_device(d_in, st, steps, out=out, scratch=scr, params=prm, trace=True)
 print(tr)
