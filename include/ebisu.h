@@ -96,7 +96,9 @@ typedef struct ebisu_params {
                                 0 = auto); the GPU tile is chosen by the planner */
   int32_t device_tile_grid[2];
   int32_t lazy;              /* accepted for parity; the GPU kernels sync once per advance */
-  int32_t exact;             /* 1: bitwise (no FMA contraction); 0: FMA chain      */
+  int32_t exact;             /* 1: bitwise (no FMA contraction); 0: tolerance mode
+                                (1e-12 relative): FMA chains, or for uniform
+                                coefficients reassociated sums (see below)         */
   int32_t persistent;        /* 1: one cooperative launch, grid sync between epochs */
   int32_t validate_tile;     /* 1: apply the reference TilingParams.validate rules  */
   int32_t lane_cells;        /* cells per lane along the fastest axis (0 = planner) */
@@ -116,7 +118,12 @@ typedef struct ebisu_params {
  * the cell only, so the kernels compute it once per cell and level and every
  * tap reuses it.  The sums keep the reference order, so the result is still
  * bitwise equal to reference_run; only the DMUL count drops (13 -> 7 DP ops
- * per j3d7pt cell-step).  per_tap_products=1 forces the per-tap kernels. */
+ * per j3d7pt cell-step).  per_tap_products=1 forces the per-tap kernels.
+ *
+ * Reassociated sums (exact = 0, uniform coefficients): sum_k c*x_k is computed
+ * as c * (regrouped sum) -- separable column/row sums shared between
+ * neighbouring targets -- within the north star's 1e-12 relative tolerance:
+ * j3d27pt 27 -> ~6 DP per cell-step, j2d25pt 25 -> ~6, j2ds25pt 25 -> ~12. */
 
 /* Closed-form execution counters of the GPU run (reference ExecutionTrace,
  * engine/trace.py:25-40), plus GPU facts. */
@@ -136,8 +143,15 @@ typedef struct ebisu_trace {
   int32_t t_used;            /* temporal depth actually fused                      */
   int32_t grid_ctas;
   int32_t warps_per_cta;
-  int32_t reserved[4];
+  int32_t arith;             /* EBISU_ARITH_*: arithmetic of the main stage        */
+  int32_t reserved[3];
 } ebisu_trace;
+
+/* ebisu_trace.arith */
+#define EBISU_ARITH_SHARED_PRODUCTS 0 /* bitwise: RN(c*x) once per cell, tap-order adds */
+#define EBISU_ARITH_PER_TAP_EXACT 1   /* bitwise: RN(ck*xk) per tap, tap-order adds     */
+#define EBISU_ARITH_PER_TAP_FMA 2     /* tolerance: FMA chain in tap order              */
+#define EBISU_ARITH_REASSOCIATED 3    /* tolerance: c * (regrouped sum), uniform coeffs */
 
 /* Library / device facts. */
 EBISU_API int32_t ebisu_abi_version(void);

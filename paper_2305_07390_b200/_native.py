@@ -101,7 +101,8 @@ class TraceC(ctypes.Structure):
         ("t_used", ctypes.c_int32),
         ("grid_ctas", ctypes.c_int32),
         ("warps_per_cta", ctypes.c_int32),
-        ("reserved", ctypes.c_int32 * 4),
+        ("arith", ctypes.c_int32),
+        ("reserved", ctypes.c_int32 * 3),
     ]
 
     def to_dict(self) -> dict:
@@ -173,6 +174,10 @@ def available() -> bool:
 
 def last_error() -> str:
     return load().ebisu_last_error().decode(errors="replace")
+
+
+# ebisu_trace.arith (include/ebisu.h EBISU_ARITH_*)
+ARITH_NAMES = {0: "shared_products", 1: "per_tap_exact", 2: "per_tap_fma", 3: "reassociated"}
 
 
 def kernel_name(kid: int) -> str:

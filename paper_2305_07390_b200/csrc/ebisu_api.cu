@@ -252,9 +252,11 @@ enum KernelId : int {
 // the planner's default lane width first -- or the one with lane width C.
 // Kernel family for a request: shared-product kernels (uni) are bitwise exact,
 // so they serve both exact and FMA requests when the coefficients are uniform.
+// Tolerance requests (exact = 0) with uniform coefficients prefer the
+// reassociated kernels (uni && !exact) and fall back to the bitwise ones.
 bool family_ok(const TbKernel& k, bool exact, bool uni, int family, int elem) {
   if (k.family != family || k.elem != elem) return false;
-  if (uni) return k.uni != 0;
+  if (uni) return k.uni != 0 && (exact ? k.exact != 0 : true);
   return k.uni == 0 && (k.exact != 0) == exact;
 }
 
@@ -262,9 +264,15 @@ const TbKernel* find_tb(int shape_id, int dims, int T, bool exact, bool uni, int
                         int elem, int C = 0, int variant = 0) {
   int n = 0;
   const TbKernel* ks = tb_kernels(&n);
-  for (int i = 0; i < n; ++i)
-    if (ks[i].shape_id == shape_id && ks[i].dims == dims && ks[i].T == T &&
-        family_ok(ks[i], exact, uni, family, elem) && (C == 0 || ks[i].C == C)) {
+  // tolerance + uniform: reassociated kernels (exact == 0) first, then the
+  // bitwise shared-product ones; variants are numbered across both passes
+  const bool tol = uni && !exact;
+  for (int pass = tol ? 0 : 1; pass < 2; ++pass)
+    for (int i = 0; i < n; ++i) {
+      if (!(ks[i].shape_id == shape_id && ks[i].dims == dims && ks[i].T == T &&
+            family_ok(ks[i], exact, uni, family, elem) && (C == 0 || ks[i].C == C)))
+        continue;
+      if (tol && (ks[i].exact == 0) != (pass == 0)) continue;
       if (variant-- == 0) return &ks[i];
     }
   return nullptr;
@@ -300,6 +308,17 @@ bool uniform_coeffs(const ProblemDesc& p) {
 }
 
 // Default fused depth (measured sweet spot on B200).
+// Tolerance mode with uniform coefficients (reassociated kernels): the
+// measured-best depth per shape where it differs from the bitwise one
+// (8192^2 x 96 / 512^3 x 500: j2d13pt t=2 601 vs t=3 , j2d9pt t=3 848 vs t=4 spills)
+int default_depth_tol(int shape_id, int exact_default) {
+  switch (shape_id) {
+    case SHAPE_J2D13PT: return 2;
+    case SHAPE_J2D9PT: return 3;
+    default: return exact_default;
+  }
+}
+
 int default_depth(int shape_id) {
   switch (shape_id) {
     case SHAPE_J2D5PT: return 8;
@@ -327,7 +346,14 @@ struct Counters {
   uint64_t gm_loads = 0, gm_stores = 0, cells_computed = 0, device_tiles = 0, syncs_device = 0,
            syncs_block = 0, launches = 0, halo_loads = 0, halo_stores = 0;
   int grid = 0, nw = 0, t_used = 0, kid = KID_NONE;
+  int arith = -1;  // EBISU_ARITH_* of the first (main) stage
 };
+
+// arithmetic family of a kernel (ebisu_trace.arith)
+inline int arith_of(const TbKernel* k) {
+  if (k->uni) return k->exact ? EBISU_ARITH_SHARED_PRODUCTS : EBISU_ARITH_REASSOCIATED;
+  return k->exact ? EBISU_ARITH_PER_TAP_EXACT : EBISU_ARITH_PER_TAP_FMA;
+}
 
 inline int stream3d_advances_host(int ka, int r1, int TZ, int WN) {
   const int n = r1 + TZ - ka;
@@ -521,6 +547,7 @@ int run_tb2d_stage(const ProblemDesc& p, const TbKernel* k, int epochs, int firs
   ctr->grid = grid;
   ctr->nw = k->NW;
   ctr->t_used = std::max(ctr->t_used, T);
+  if (ctr->arith < 0) ctr->arith = arith_of(k);
   if (ctr->kid == KID_NONE) ctr->kid = KID_STREAM2D;  // the first (main) stage names the run
   return EBISU_OK;
 }
@@ -619,6 +646,7 @@ int run_halo2d_stage(const ProblemDesc& p, const TbKernel* k, int epochs, int fi
   ctr->grid = grid;
   ctr->nw = k->NW;
   ctr->t_used = std::max(ctr->t_used, T);
+  if (ctr->arith < 0) ctr->arith = arith_of(k);
   if (ctr->kid == KID_NONE) ctr->kid = KID_HALO2D;
   return EBISU_OK;
 }
@@ -735,6 +763,7 @@ int run_tb3d_stage(const ProblemDesc& p, const TbKernel* k, int epochs, int firs
   ctr->grid = grid;
   ctr->nw = k->NW;
   ctr->t_used = std::max(ctr->t_used, T);
+  if (ctr->arith < 0) ctr->arith = arith_of(k);
   if (ctr->kid == KID_NONE) ctr->kid = KID_STREAM3D;
   return EBISU_OK;
 }
@@ -777,6 +806,7 @@ int run_device_impl(const ProblemDesc& p0, const void* d_in, void* d_out, void* 
   bool tb_ok = tb_shape && (tma_direct || pitched);
   if (tb_ok) {
     int t = (prm && prm->t > 0) ? prm->t : default_depth(p.shape_id);
+    if (!(prm && prm->t > 0) && uni && !exact) t = default_depth_tol(p.shape_id, t);
     // fp32 windows cost half the registers: the 2-D star runs deeper
     if (!(prm && prm->t > 0) && p.elem == 4 && p.shape_id == SHAPE_J2D5PT) t = 16;
     const int want_c = prm ? prm->lane_cells : 0;
@@ -917,6 +947,7 @@ int run_device_impl(const ProblemDesc& p0, const void* d_in, void* d_out, void* 
       ctr->gm_loads += (uint64_t)s.epochs * (uint64_t)total;
       ctr->gm_stores += (uint64_t)s.epochs * (uint64_t)total;
       ctr->cells_computed += (uint64_t)s.epochs * (uint64_t)total;
+      if (ctr->arith < 0) ctr->arith = exact ? EBISU_ARITH_PER_TAP_EXACT : EBISU_ARITH_PER_TAP_FMA;
       if (ctr->kid == KID_NONE) ctr->kid = KID_NAIVE;
       ctr->t_used = std::max(ctr->t_used, 1);
       src = (s.epochs % 2 == 1) ? dst : (dst == BUF_OUT ? BUF_SCR : BUF_OUT);
@@ -1021,6 +1052,7 @@ static void fill_trace(ebisu_trace* tr, const ProblemDesc& p, long long steps, c
   tr->t_used = c.t_used;
   tr->grid_ctas = c.grid;
   tr->warps_per_cta = c.nw;
+  tr->arith = c.arith < 0 ? EBISU_ARITH_SHARED_PRODUCTS : c.arith;
 }
 
 static int32_t run_device_entry(const ebisu_stencil* stencil, int32_t ndim,

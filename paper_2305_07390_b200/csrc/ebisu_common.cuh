@@ -76,6 +76,31 @@ __device__ __forceinline__ double ld_shared_if(const double* p, bool pred, doubl
   return r;
 }
 
+// two adjacent cells to global memory, branch free: one 16-byte store when
+// both are stored, else the single one (p must be 16-byte aligned)
+__device__ __forceinline__ void st_pair_if(double* p, double a, double b, bool s0, bool s1) {
+  asm volatile(
+      "{\n\t.reg .pred p0, p1, pb, q0, q1;\n\t"
+      "setp.ne.b32 p0, %3, 0;\n\tsetp.ne.b32 p1, %4, 0;\n\t"
+      "and.pred pb, p0, p1;\n\txor.pred q0, p0, pb;\n\txor.pred q1, p1, pb;\n\t"
+      "@pb st.global.v2.f64 [%0], {%1, %2};\n\t"
+      "@q0 st.global.f64 [%0], %1;\n\t"
+      "@q1 st.global.f64 [%0+8], %2;\n\t}" ::"l"(p),
+      "d"(a), "d"(b), "r"((int)s0), "r"((int)s1)
+      : "memory");
+}
+__device__ __forceinline__ void st_pair_if(float* p, float a, float b, bool s0, bool s1) {
+  asm volatile(
+      "{\n\t.reg .pred p0, p1, pb, q0, q1;\n\t"
+      "setp.ne.b32 p0, %3, 0;\n\tsetp.ne.b32 p1, %4, 0;\n\t"
+      "and.pred pb, p0, p1;\n\txor.pred q0, p0, pb;\n\txor.pred q1, p1, pb;\n\t"
+      "@pb st.global.v2.f32 [%0], {%1, %2};\n\t"
+      "@q0 st.global.f32 [%0], %1;\n\t"
+      "@q1 st.global.f32 [%0+4], %2;\n\t}" ::"l"(p),
+      "f"(a), "f"(b), "r"((int)s0), "r"((int)s1)
+      : "memory");
+}
+
 // ---- epoch dataflow flags (gpu scope) --------------------------------------
 __device__ __forceinline__ int ld_acquire_gpu(const int* p) {
   int v;
@@ -163,6 +188,16 @@ __device__ __forceinline__ double add_rn<double>(double a, double b) {
 template <>
 __device__ __forceinline__ float add_rn<float>(float a, float b) {
   return __fadd_rn(a, b);
+}
+template <class E>
+__device__ __forceinline__ E sub_rn(E a, E b);
+template <>
+__device__ __forceinline__ double sub_rn<double>(double a, double b) {
+  return __dsub_rn(a, b);
+}
+template <>
+__device__ __forceinline__ float sub_rn<float>(float a, float b) {
+  return __fsub_rn(a, b);
 }
 template <class E>
 __device__ __forceinline__ E fma_rn(E a, E b, E c);

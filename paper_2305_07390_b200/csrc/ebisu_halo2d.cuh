@@ -293,12 +293,134 @@ __device__ __forceinline__ int halo2d_unit(const CUtensorMap* tm, double* __rest
     }
   };
 
+  // Tolerance mode (exact = 0, uniform coefficients), stars with Z = R >= U:
+  // level-major blocks of U advances (see stream2d_unit's block_ra) -- the
+  // column sums of a level's U targets share partial sums (slide4), the row
+  // sums of each centre row are sliding sums over the lane's C cells plus the
+  // exchanged halo.  Every exchanged centre row is >= Z - U + 1 advances old,
+  // so one barrier wait per block (for advance adv + U - 1 - DR) covers it.
+  constexpr bool RA = UNI && !EXACT;
+  static_assert(!RA || (SHIFT == 4 && SH::kStar && Z >= SHIFT), "tolerance halo kernel: stars, Z >= U");
+  auto block_ra = [&](int kbase, auto frows_tag) {
+    constexpr bool FROWS = decltype(frows_tag)::value;
+    constexpr int U = SHIFT;
+    if (adv + U - 1 >= (uint32_t)Cfg::DR) {
+      const uint32_t a = adv + U - 1 - Cfg::DR;
+      mbar_wait(&advbar[a % Cfg::DR], (a / Cfg::DR) & 1);
+    }
+#pragma unroll
+    for (int uu = 0; uu < U; ++uu) {
+      const int k = kbase + uu;
+      const uint32_t pos = ring_cnt + (uint32_t)(k - ka);
+      const uint32_t slot = pos & (S - 1);
+      mbar_wait(&bars[slot], (pos / S) & 1);
+      if (lane == 0 && k > ka && k - 1 + S < kend) {
+        const uint32_t ps = (pos - 1) & (S - 1);
+        mbar_arrive_expect_tx(&bars[ps], ROW_BYTES);
+        tma_load_2d(ring + ps * LC, tm, XW, k - 1 + S, &bars[ps]);
+      }
+      const double* rowp = ring + slot * LC + lane * C;
+      double v[C];
+#pragma unroll
+      for (int c = 0; c < C; c += 2) {
+        const double2 t2 = *reinterpret_cast<const double2*>(rowp + c);
+        v[c] = __dmul_rn(cf.c[0], t2.x);
+        v[c + 1] = __dmul_rn(cf.c[0], t2.y);
+      }
+#pragma unroll
+      for (int c = 0; c < C; ++c) win[0][W - 1 + uu][c] = v[c];
+      push(0, k & (NB - 1), v);
+    }
+    static_for<T>([&](auto sI) {
+      constexpr int s = decltype(sI)::value + 1;
+      double V[U][C];
+#pragma unroll
+      for (int c = 0; c < C; ++c) {
+        double a[W + 3], o[4];
+#pragma unroll
+        for (int j = 0; j < W + 3; ++j) a[j] = win[s - 1][j][c];
+        slide4<W>(a, o);
+#pragma unroll
+        for (int uu = 0; uu < U; ++uu) V[uu][c] = o[uu];
+      }
+#pragma unroll
+      for (int uu = 0; uu < U; ++uu) {
+        const int k = kbase + uu;
+        const int q = k - s * Z;
+        // centre row q of level s-1 with R columns each side: in-warp by
+        // shuffles, across warps from the neighbours' edge buffers
+        double b[2 * R + C];
+#pragma unroll
+        for (int c = 0; c < C; ++c) b[R + c] = win[s - 1][R + uu][c];
+        const int xs = (k - Z) & (NB - 1);
+        const double* Lb = xrow(s - 1, xs, wr, 0);
+        const double* Rb = xrow(s - 1, xs, wl, 1);
+        static_for<R>([&](auto jI) {
+          constexpr int j = decltype(jI)::value;
+          constexpr int ccl = -R + j;
+          constexpr int dl = (-ccl + C - 1) / C;
+          constexpr int coll = ccl + dl * C;
+          constexpr int ccr = C + j;
+          constexpr int dr = ccr / C;
+          constexpr int colr = ccr - dr * C;
+          double x0 = __shfl_up_sync(kFullMask, b[R + coll], dl);
+          double x1 = __shfl_down_sync(kFullMask, b[R + colr], dr);
+          b[j] = ld_shared_if(Rb + max(R + lane * C + ccl, 0), lane < dl, x0);
+          b[R + C + j] = ld_shared_if(Lb + min(max(lane * C + ccr - LC, 0), R - 1), lane > 31 - dr, x1);
+        });
+        double h[C];
+        slide_n<W, C>(b, h);
+        bool frow = false;
+        if constexpr (FROWS) frow = (q < R) || (q >= n0 - R);
+        double nv[C];
+#pragma unroll
+        for (int c = 0; c < C; ++c) {
+          const double centre = b[R + c];
+          const double acc = __dadd_rn(V[uu][c], __dsub_rn(h[c], centre));
+          const double val = s < T ? __dmul_rn(cf.c[0], acc) : acc;
+          bool f = frow;
+          if constexpr (EDGE) f = f || ((fmask >> c) & 1u);
+          nv[c] = f ? centre : val;
+        }
+        if constexpr (s < T) {
+#pragma unroll
+          for (int c = 0; c < C; ++c) win[s][W - 1 + uu][c] = nv[c];
+          push(s, k & (NB - 1), nv);
+        } else if (q >= r0 && q < r1 && !frow) {
+          double* orow = out + (size_t)q * (size_t)pitch + (XW + lane * C);
+#pragma unroll
+          for (int c = 0; c < C; c += 2)
+            st_pair_if(orow + c, nv[c], nv[c + 1], (stmask >> c) & 1u, (stmask >> (c + 1)) & 1u);
+        }
+      }
+    });
+    __syncwarp();
+    if (lane == 0)
+#pragma unroll
+      for (int uu = 0; uu < U; ++uu) mbar_arrive(&advbar[(adv + uu) % Cfg::DR]);
+    adv += U;
+#pragma unroll
+    for (int L = 0; L < T; ++L)
+#pragma unroll
+      for (int w = 0; w + 1 < W; ++w)
+#pragma unroll
+        for (int c = 0; c < C; ++c) win[L][w][c] = win[L][w + U][c];
+  };
+
   for (int kbase = ka; kbase < kend; kbase += UW) {
     // target rows of this block: [kbase - TZ, kbase + UW - 1 - Z]
-    if ((kbase - TZ < R) || (kbase + UW - 1 - Z >= n0 - R))
-      block(kbase, std::true_type{});
-    else
-      block(kbase, std::false_type{});
+    const bool frows = (kbase - TZ < R) || (kbase + UW - 1 - Z >= n0 - R);
+    if constexpr (RA) {
+      if (frows)
+        block_ra(kbase, std::true_type{});
+      else
+        block_ra(kbase, std::false_type{});
+    } else {
+      if (frows)
+        block(kbase, std::true_type{});
+      else
+        block(kbase, std::false_type{});
+    }
   }
   return nadv;
 }

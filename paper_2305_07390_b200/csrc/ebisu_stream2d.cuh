@@ -164,6 +164,83 @@ __host__ __device__ constexpr int pmod(int a) {
   return ((a % W) + W) % W;
 }
 
+
+// ---- tolerance mode (exact = 0, uniform coefficients): reassociated sums ----
+// sum_k c*x_k = c * sum_k x_k may be regrouped within the north star's fp64
+// tolerance (1e-12 relative).  Stars: sum = column sum over 2R+1 rows + row
+// sum over 2R+1 columns - centre; boxes: row sum of the column sums.  Both
+// are sliding sums of K = 2R+1 terms for 4 consecutive outputs (4 target
+// rows of a block, 4 cells of a lane), computed with shared partial sums:
+// K + 4 adds for 4 outputs instead of 4(K-1), no subtraction, no drift.
+// j2ds25pt: 11.5 DP per cell-step instead of 25.
+template <class SH>
+__host__ __device__ constexpr bool ra2d_star() {
+  // star pattern in reference order: column -R..R then row offsets
+  if (!SH::kStar || SH::dims != 2) return false;
+  return true;
+}
+template <class SH>
+__host__ __device__ constexpr bool ra2d_box() {
+  return !SH::kStar && SH::dims == 2 && SH::NT == (2 * SH::R + 1) * (2 * SH::R + 1);
+}
+template <class SH>
+__host__ __device__ constexpr bool ra2d_eligible() {
+  return ra2d_star<SH>() || ra2d_box<SH>();
+}
+// pairwise sum of a[0..N-1] (short dependency chains)
+template <int N, class E>
+__device__ __forceinline__ E tree_sum(const E* a) {
+  E part[N];
+#pragma unroll
+  for (int j = 0; j < N; ++j) part[j] = a[j];
+#pragma unroll
+  for (int w = 1; w < N; w *= 2)
+#pragma unroll
+    for (int j = 0; j + w < N; j += 2 * w) part[j] = add_rn<E>(part[j], part[j + w]);
+  return part[0];
+}
+// o[i] = a[i] + ... + a[i+K-1], i = 0..1 (a has K+1 entries): K adds
+template <int K, class E>
+__device__ __forceinline__ void slide2(const E* a, E* o) {
+  const E core = tree_sum<K - 1>(a + 1);
+  o[0] = add_rn<E>(a[0], core);
+  o[1] = add_rn<E>(core, a[K]);
+}
+// o[i] = a[i] + ... + a[i+K-1], i = 0..3 (a has K+3 entries)
+template <int K, class E>
+__device__ __forceinline__ void slide4(const E* a, E* o) {
+  static_assert(K >= 3, "window of at least 3");
+  E core = E(0);
+  if constexpr (K > 3) {
+    // a[3..K-1], pairwise (short dependency chains)
+    E part[(K - 3 + 1) / 2];
+#pragma unroll
+    for (int j = 0; j < (K - 3) / 2; ++j) part[j] = add_rn<E>(a[3 + 2 * j], a[4 + 2 * j]);
+    if constexpr ((K - 3) % 2) part[(K - 3) / 2] = a[K - 1];
+    constexpr int NP = (K - 3 + 1) / 2;
+#pragma unroll
+    for (int w = 1; w < NP; w *= 2)
+#pragma unroll
+      for (int j = 0; j + w < NP; j += 2 * w) part[j] = add_rn<E>(part[j], part[j + w]);
+    core = part[0];
+  }
+  const E l1 = K > 3 ? add_rn<E>(core, a[2]) : a[2];
+  const E l2 = add_rn<E>(l1, a[1]);
+  o[0] = add_rn<E>(l2, a[0]);
+  o[1] = add_rn<E>(l2, a[K]);
+  const E p = add_rn<E>(a[K], a[K + 1]);
+  o[2] = add_rn<E>(l1, p);
+  o[3] = add_rn<E>(K > 3 ? add_rn<E>(core, p) : p, a[K + 2]);
+}
+template <int K, int N, class E>
+__device__ __forceinline__ void slide_n(const E* a, E* o) {
+  static_assert(N == 2 || N == 4, "2 or 4 outputs");
+  if constexpr (N == 2)
+    slide2<K>(a, o);
+  else
+    slide4<K>(a, o);
+}
+
 // One work unit (warp strip x row segment) of one epoch.  FC selects the
 // frame-column handling (see StripGeom); frame rows are handled per block.
 template <class SH, int T, int C, int S, bool EXACT, bool UNI, int FC, class E, int SHIFT = 0>
@@ -239,6 +316,9 @@ __device__ __forceinline__ int stream2d_unit(const CUtensorMap* tm, E* __restric
   //     the instruction cache (the rotating kernel measured 11.6 %
   //     no-instruction stalls at R = 6).
   constexpr int UW = SHIFT ? SHIFT : W;
+  // tolerance mode (exact = 0, uniform coefficients): reassociated sums
+  constexpr bool RA = UNI && !EXACT;
+  static_assert(!RA || C == 4, "reassociated kernels: 4 cells per lane");
   auto slot_of = [](int uu, int s, int dy) {
     return SHIFT ? R + dy + uu : pmod<W>(uu - s * R + dy);
   };
@@ -305,7 +385,7 @@ __device__ __forceinline__ int stream2d_unit(const CUtensorMap* tm, E* __restric
         E hl[W][R], hr[W][R];
         static_for<W>([&](auto wI) {
           constexpr int dy = decltype(wI)::value - R;
-          if constexpr (row_has_halo<SH>(dy)) {
+          if constexpr (!RA && row_has_halo<SH>(dy)) {
             static_for<R>([&](auto jI) {
               constexpr int j = decltype(jI)::value;
               constexpr int ccl = -R + j;
@@ -322,6 +402,40 @@ __device__ __forceinline__ int stream2d_unit(const CUtensorMap* tm, E* __restric
         });
         // tap-major order: the C per-column chains are independent
         E acc[C];
+        if constexpr (RA) {
+          // tolerance mode: column sums over the 2R+1 window rows (pairwise),
+          // then 2R+1-column row sums of the centre row (stars, + column sum
+          // - centre) or of the column sums (boxes), see slide4
+          E b[2 * R + C];
+#pragma unroll
+          for (int c = 0; c < C; ++c) {
+            E part[W];
+#pragma unroll
+            for (int j = 0; j < W; ++j) part[j] = win[s - 1][slot_of(uu, s, j - R)][c];
+#pragma unroll
+            for (int w = 1; w < W; w *= 2)
+#pragma unroll
+              for (int j = 0; j + w < W; j += 2 * w) part[j] = add_rn<E>(part[j], part[j + w]);
+            acc[c] = part[0];
+            b[R + c] = ra2d_box<SH>() ? part[0] : win[s - 1][slot_of(uu, s, 0)][c];
+          }
+          static_for<R>([&](auto jI) {
+            constexpr int j = decltype(jI)::value;
+            constexpr int ccl = -R + j;
+            constexpr int dl = (-ccl + C - 1) / C;
+            constexpr int coll = ccl + dl * C;
+            constexpr int ccr = C + j;
+            constexpr int dr = ccr / C;
+            constexpr int colr = ccr - dr * C;
+            b[j] = __shfl_up_sync(kFullMask, b[R + coll], dl);
+            b[R + C + j] = __shfl_down_sync(kFullMask, b[R + colr], dr);
+          });
+          E h[4];
+          slide4<W>(b, h);
+#pragma unroll
+          for (int c = 0; c < C; ++c)
+            acc[c] = ra2d_box<SH>() ? h[c] : add_rn<E>(acc[c], sub_rn<E>(h[c], b[R + c]));
+        } else
         static_for<SH::NT>([&](auto iI) {
           constexpr int i = decltype(iI)::value;
           constexpr Off o = SH::tap(i);
@@ -369,14 +483,23 @@ __device__ __forceinline__ int stream2d_unit(const CUtensorMap* tm, E* __restric
         } else {
           if (q >= r0 && q < r1) {
             E* orow = out + (size_t)q * (size_t)pitch + (X0 + lane * C);
+            bool st[C];
 #pragma unroll
             for (int c = 0; c < C; ++c) {
-              bool st = stcol[c];
+              st[c] = stcol[c];
               if constexpr (UNI) {
-                if (FROWS) st = st && !frow;
-                if (col_may_frame(c)) st = st && !fcol[c];
+                if (FROWS) st[c] = st[c] && !frow;
+                if (col_may_frame(c)) st[c] = st[c] && !fcol[c];
               }
-              if (st) orow[c] = nv[c];
+            }
+            if constexpr (C % 2 == 0) {
+              // 16-byte stores (branch free; a pair is split only at strip edges)
+#pragma unroll
+              for (int c = 0; c < C; c += 2) st_pair_if(orow + c, nv[c], nv[c + 1], st[c], st[c + 1]);
+            } else {
+#pragma unroll
+              for (int c = 0; c < C; ++c)
+                if (st[c]) orow[c] = nv[c];
             }
           }
         }
@@ -393,13 +516,121 @@ __device__ __forceinline__ int stream2d_unit(const CUtensorMap* tm, E* __restric
     }
   };
 
+  // Tolerance mode with shifted windows (large radii): level-major blocks of
+  // U = 4 advances -- level 0 loads the block's 4 rows, then each level
+  // completes its 4 target rows from the window (the same rows the
+  // advance-major order uses), sharing the column sums of the 4 targets.
+  auto block_ra = [&](int kbase, auto frows_tag) {
+    constexpr bool FROWS = decltype(frows_tag)::value;
+    static_assert(!(RA && SHIFT) || SHIFT == 4, "level-major blocks of 4 rows");
+#pragma unroll
+    for (int uu = 0; uu < UW; ++uu) {
+      const int k = kbase + uu;
+      const uint32_t pos = ring_cnt + (uint32_t)(k - ka);
+      const uint32_t slot = pos & (S - 1);
+      mbar_wait(&bars[slot], (pos / S) & 1);
+      if (lane == 0 && k > ka && k - 1 + S < kload) {
+        const uint32_t ps = (pos - 1) & (S - 1);
+        mbar_arrive_expect_tx(&bars[ps], ROW_BYTES);
+        tma_load_2d(ring + ps * LC, tm, X0, k - 1 + S, &bars[ps]);
+      }
+      const E* rowp = ring + slot * LC + lane * C;
+#pragma unroll
+      for (int c = 0; c < C; c += 2) {
+        const vec2_t<E> t2 = *reinterpret_cast<const vec2_t<E>*>(rowp + c);
+        win[0][W - 1 + uu][c] = mul_rn<E>(cf.c[0], t2.x);
+        win[0][W - 1 + uu][c + 1] = mul_rn<E>(cf.c[0], t2.y);
+      }
+    }
+    static_for<T>([&](auto sI) {
+      constexpr int s = decltype(sI)::value + 1;
+      E acc[UW][C];
+      // column sums of the 4 targets (window slots uu .. uu+2R)
+      E V[UW][C];
+#pragma unroll
+      for (int c = 0; c < C; ++c) {
+        E a[W + 3], o[4];
+#pragma unroll
+        for (int j = 0; j < W + 3; ++j) a[j] = win[s - 1][j][c];
+        slide4<W>(a, o);
+#pragma unroll
+        for (int uu = 0; uu < UW; ++uu) V[uu][c] = o[uu];
+      }
+#pragma unroll
+      for (int uu = 0; uu < UW; ++uu) {
+        // row sums over 2R+1 columns of the centre row (stars) or of the
+        // column sums (boxes); neighbours outside the lane by shuffles
+        E b[2 * R + C];
+#pragma unroll
+        for (int c = 0; c < C; ++c) b[R + c] = ra2d_box<SH>() ? V[uu][c] : win[s - 1][R + uu][c];
+        static_for<R>([&](auto jI) {
+          constexpr int j = decltype(jI)::value;
+          constexpr int ccl = -R + j;
+          constexpr int dl = (-ccl + C - 1) / C;
+          constexpr int coll = ccl + dl * C;
+          constexpr int ccr = C + j;
+          constexpr int dr = ccr / C;
+          constexpr int colr = ccr - dr * C;
+          b[j] = __shfl_up_sync(kFullMask, b[R + coll], dl);
+          b[R + C + j] = __shfl_down_sync(kFullMask, b[R + colr], dr);
+        });
+        E h[4];
+        slide4<W>(b, h);
+#pragma unroll
+        for (int c = 0; c < C; ++c)
+          acc[uu][c] = ra2d_box<SH>() ? h[c]
+                                      : add_rn<E>(V[uu][c], sub_rn<E>(h[c], win[s - 1][R + uu][c]));
+      }
+#pragma unroll
+      for (int uu = 0; uu < UW; ++uu) {
+        const int q = kbase + uu - s * R;
+        bool frow = false;
+        if constexpr (FROWS) frow = (q < R) || (q >= n0 - R);
+        E nv[C];
+#pragma unroll
+        for (int c = 0; c < C; ++c) {
+          const E centre = win[s - 1][R + uu][c];
+          const E val = s < T ? mul_rn<E>(cf.c[0], acc[uu][c]) : acc[uu][c];
+          bool f = frow;
+          if (col_may_frame(c)) f = f || fcol[c];
+          nv[c] = f ? centre : val;
+        }
+        if constexpr (s < T) {
+#pragma unroll
+          for (int c = 0; c < C; ++c) win[s][W - 1 + uu][c] = nv[c];
+        } else if (q >= r0 && q < r1 && !frow) {
+          E* orow = out + (size_t)q * (size_t)pitch + (X0 + lane * C);
+#pragma unroll
+          for (int c = 0; c < C; c += 2) {
+            const bool s0 = stcol[c] && !(col_may_frame(c) && fcol[c]);
+            const bool s1 = stcol[c + 1] && !(col_may_frame(c + 1) && fcol[c + 1]);
+            st_pair_if(orow + c, nv[c], nv[c + 1], s0, s1);
+          }
+        }
+      }
+    });
+#pragma unroll
+    for (int L = 0; L < T; ++L)
+#pragma unroll
+      for (int w = 0; w + 1 < W; ++w)
+#pragma unroll
+        for (int c = 0; c < C; ++c) win[L][w][c] = win[L][w + SHIFT][c];
+  };
+
   for (int kbase = ka; kbase < kend; kbase += UW) {
     // target rows of this block: [kbase - TR, kbase + UW - 1 - R]
     const bool frows = (kbase - TR < R) || (kbase + UW - 1 >= n0);
-    if (frows)
-      block(kbase, std::true_type{});
-    else
-      block(kbase, std::false_type{});
+    if constexpr (RA && SHIFT) {
+      if (frows)
+        block_ra(kbase, std::true_type{});
+      else
+        block_ra(kbase, std::false_type{});
+    } else {
+      if (frows)
+        block(kbase, std::true_type{});
+      else
+        block(kbase, std::false_type{});
+    }
   }
   return kload - ka;
 }
@@ -484,8 +715,13 @@ __global__ void __launch_bounds__(NW * 32, MINB)
         asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_start));
       int used;
       if constexpr (R > C) {
-        used = stream2d_unit<SH, T, C, S, EXACT, UNI, 3, E, SHIFT>(tm, out, ring, bars, ring_cnt,
-                                                                   lane, n0, n1, a.pitch, g, r0, r1, cf);
+        // generic strips; those clear of the frame columns skip the masks
+        if (g.X0 >= R && g.X0 + Cfg::LC <= n1 - R)
+          used = stream2d_unit<SH, T, C, S, EXACT, UNI, 0, E, SHIFT>(tm, out, ring, bars, ring_cnt,
+                                                                     lane, n0, n1, a.pitch, g, r0, r1, cf);
+        else
+          used = stream2d_unit<SH, T, C, S, EXACT, UNI, 3, E, SHIFT>(tm, out, ring, bars, ring_cnt,
+                                                                     lane, n0, n1, a.pitch, g, r0, r1, cf);
       } else switch (g.fc) {
         case 0:
           used = stream2d_unit<SH, T, C, S, EXACT, UNI, 0, E, SHIFT>(tm, out, ring, bars, ring_cnt,

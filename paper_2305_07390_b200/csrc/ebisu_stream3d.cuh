@@ -614,6 +614,46 @@ __device__ __forceinline__ int stream3d_unit_ps(const CUtensorMap* tm, E* __rest
 // reference order.  A level keeps two partial sums, the plane it will consume
 // next and the plane it consumed last (frame carry): no 3-plane neighbourhood
 // per advance, a third of the shuffles and halo loads of the window path.
+
+// ---- tolerance mode (exact = 0, uniform coefficients): reassociated sums ----
+// With one coefficient c for every tap, sum_k c*x_k = c * sum_k x_k, and the
+// sum may be regrouped: the north star's fp64 tolerance (1e-12 relative)
+// admits any order.  A plane's in-plane taps are then a "pattern" sum that
+// is the same for every target the plane feeds (j3d27pt: the 3x3 box for all
+// three targets), computed ONCE per plane as separable column sums: 6 DP per
+// j3d27pt cell-step instead of 27.
+//   pat3_mask(dz): 9-bit mask of the in-plane offsets (d1, d2) with d0 = dz
+//   pat3_col(dz, dx): 3-bit set of rows d1 in column d2 = dx of that pattern
+template <class SH>
+__host__ __device__ constexpr uint32_t pat3_mask(int dz) {
+  uint32_t m = 0;
+  for (int i = 0; i < SH::NT; ++i)
+    if (SH::tap(i).d0 == dz) m |= 1u << ((SH::tap(i).d1 + 1) * 3 + (SH::tap(i).d2 + 1));
+  return m;
+}
+template <class SH>
+__host__ __device__ constexpr int pat3_col(int dz, int dx) {
+  int s = 0;
+  for (int dy = -1; dy <= 1; ++dy)
+    if ((pat3_mask<SH>(dz) >> ((dy + 1) * 3 + (dx + 1))) & 1u) s |= 1 << (dy + 1);
+  return s;
+}
+// column sum over row set RS needed at all / needed in a neighbour column
+template <class SH>
+__host__ __device__ constexpr bool pat3_rs_used(int rs, bool shifted) {
+  for (int dz = -1; dz <= 1; ++dz)
+    for (int dx = -1; dx <= 1; ++dx)
+      if (pat3_col<SH>(dz, dx) == rs && (!shifted || dx != 0)) return true;
+  return false;
+}
+// first dz with the same pattern (pattern sums are computed once)
+template <class SH>
+__host__ __device__ constexpr int pat3_canon(int dz) {
+  for (int d = -1; d < dz; ++d)
+    if (pat3_mask<SH>(d) == pat3_mask<SH>(dz)) return d;
+  return dz;
+}
+
 template <class SH>
 __host__ __device__ constexpr bool pm_eligible() {
   if (SH::dims != 3 || SH::R != 1 || SH::kStar) return false;
@@ -720,10 +760,146 @@ __device__ __forceinline__ int stream3d_unit_pm(const CUtensorMap* tm, E* __rest
     return acc;
   };
 
+  // Tolerance mode: level s consumes plane p (the level below, produced last
+  // advance) through its pattern sums -- target c-1 gets pattern(+1) and
+  // completes, target c gets pattern(0), target c+1 opens with pattern(-1).
+  constexpr bool RA = UNI && !EXACT;
+  int bk = 0, bp = 0;
+  auto ra_level = [&](auto s_tag, int q, bool fpl, E (&nw)[CY][CX]) {
+    constexpr int s = decltype(s_tag)::value;
+    // plane rows -1..CY (halo rows from the warps above / below), own columns
+    E e[CY + 2][CX];
+#pragma unroll
+    for (int cy = 0; cy < CY; ++cy)
+#pragma unroll
+      for (int cx = 0; cx < CX; ++cx) e[cy + 1][cx] = Yc[s - 1][cy][cx];
+    {
+      const E* up = hrow(s - 1, bp, wa, warp > 0 ? 1 : 0);
+      const E* dn = hrow(s - 1, bp, wbl, warp < NWY - 1 ? 0 : 1);
+#pragma unroll
+      for (int cx = 0; cx < CX; cx += 2) {
+        const vec2_t<E> a2 = *reinterpret_cast<const vec2_t<E>*>(up + cx);
+        const vec2_t<E> b2 = *reinterpret_cast<const vec2_t<E>*>(dn + cx);
+        e[0][cx] = a2.x;
+        e[0][cx + 1] = a2.y;
+        e[CY + 1][cx] = b2.x;
+        e[CY + 1][cx + 1] = b2.y;
+      }
+    }
+    // column sums cs[rs][cy][cx + 1] over row set rs (bit dy+1), own columns;
+    // neighbour columns -1 / CX by shuffles where a pattern reaches them
+    E cs[8][CY][CX + 2];
+    static_for<8>([&](auto rI) {
+      constexpr int RS = decltype(rI)::value;
+      if constexpr (RS != 0 && pat3_rs_used<SH>(RS, false)) {
+#pragma unroll
+        for (int cx = 0; cx < CX; ++cx) {
+          if constexpr (RS == 7 && CY % 2 == 0) {
+            // rows cy-1..cy+1: the pair (cy, cy+1) is shared by outputs cy, cy+1
+#pragma unroll
+            for (int cy = 0; cy < CY; cy += 2) {
+              const E m = add_rn<E>(e[cy + 1][cx], e[cy + 2][cx]);
+              cs[RS][cy][cx + 1] = add_rn<E>(e[cy][cx], m);
+              cs[RS][cy + 1][cx + 1] = add_rn<E>(m, e[cy + 3][cx]);
+            }
+          } else {
+#pragma unroll
+            for (int cy = 0; cy < CY; ++cy) {
+              E a = E(0);
+              bool first = true;
+#pragma unroll
+              for (int dy = -1; dy <= 1; ++dy)
+                if ((RS >> (dy + 1)) & 1) {
+                  a = first ? e[cy + 1 + dy][cx] : add_rn<E>(a, e[cy + 1 + dy][cx]);
+                  first = false;
+                }
+              cs[RS][cy][cx + 1] = a;
+            }
+          }
+        }
+        if constexpr (pat3_rs_used<SH>(RS, true)) {
+#pragma unroll
+          for (int cy = 0; cy < CY; ++cy) {
+            cs[RS][cy][0] = __shfl_up_sync(kFullMask, cs[RS][cy][CX], 1);
+            cs[RS][cy][CX + 1] = __shfl_down_sync(kFullMask, cs[RS][cy][1], 1);
+          }
+        }
+      }
+    });
+    // pattern sums of dz = -1, 0, +1 (identical patterns computed once)
+    E ps[3][CY][CX];
+    static_for<3>([&](auto zI) {
+      constexpr int dz = decltype(zI)::value - 1;
+      if constexpr (pat3_canon<SH>(dz) == dz && pat3_mask<SH>(dz) != 0) {
+        constexpr int c0 = pat3_col<SH>(dz, -1), c1 = pat3_col<SH>(dz, 0),
+                      c2 = pat3_col<SH>(dz, 1);
+#pragma unroll
+        for (int cy = 0; cy < CY; ++cy) {
+          if constexpr (c0 == 7 && c1 == 7 && c2 == 7 && CX % 2 == 0) {
+#pragma unroll
+            for (int cx = 0; cx < CX; cx += 2) {
+              const E m = add_rn<E>(cs[7][cy][cx + 1], cs[7][cy][cx + 2]);
+              ps[zI][cy][cx] = add_rn<E>(cs[7][cy][cx], m);
+              ps[zI][cy][cx + 1] = add_rn<E>(m, cs[7][cy][cx + 3]);
+            }
+          } else {
+#pragma unroll
+            for (int cx = 0; cx < CX; ++cx) {
+              E a = E(0);
+              bool first = true;
+              if constexpr (c1 != 0) {
+                a = cs[c1][cy][cx + 1];
+                first = false;
+              }
+              if constexpr (c0 != 0) {
+                a = first ? cs[c0][cy][cx] : add_rn<E>(a, cs[c0][cy][cx]);
+                first = false;
+              }
+              if constexpr (c2 != 0) a = first ? cs[c2][cy][cx + 2] : add_rn<E>(a, cs[c2][cy][cx + 2]);
+              ps[zI][cy][cx] = a;
+            }
+          }
+        }
+      }
+    });
+    constexpr int zm = pat3_canon<SH>(-1) + 1, z0 = pat3_canon<SH>(0) + 1,
+                  zp = pat3_canon<SH>(1) + 1;
+    E nv[CY][CX];
+#pragma unroll
+    for (int cy = 0; cy < CY; ++cy)
+#pragma unroll
+      for (int cx = 0; cx < CX; ++cx) {
+        const E Cq = pat3_mask<SH>(1) ? add_rn<E>(B[s - 1][cy][cx], ps[zp][cy][cx]) : B[s - 1][cy][cx];
+        const E Bn = pat3_mask<SH>(0) ? add_rn<E>(A[s - 1][cy][cx], ps[z0][cy][cx]) : A[s - 1][cy][cx];
+        const E An = pat3_mask<SH>(-1) ? ps[zm][cy][cx] : E(0);
+        const E val = s < T ? mul_rn<E>(cf.c[0], Cq) : Cq;
+        bool f = fpl;
+        if constexpr (EDGE) f = f || ((fmask >> (cy * CX + cx)) & 1u);
+        nv[cy][cx] = f ? Yp[s - 1][cy][cx] : val;
+        A[s - 1][cy][cx] = An;
+        B[s - 1][cy][cx] = Bn;
+        Yp[s - 1][cy][cx] = Yc[s - 1][cy][cx];
+        Yc[s - 1][cy][cx] = nw[cy][cx];
+        nw[cy][cx] = nv[cy][cx];
+      }
+    if constexpr (s < T) {
+      push(s, bk, nv);
+    } else {
+      if (q >= r0 && q < r1 && !fpl) {
+        E* o = obase + (long long)q * plane;
+#pragma unroll
+        for (int cy = 0; cy < CY; ++cy)
+#pragma unroll
+          for (int cx = 0; cx < CX; ++cx)
+            if ((stmask >> (cy * CX + cx)) & 1u) o[(long long)cy * rp + cx] = nv[cy][cx];
+      }
+    }
+  };
+
   auto advance = [&](int k, auto fpl_tag) {
     constexpr bool FPL = decltype(fpl_tag)::value;
-    const int bk = k & (NB - 1);
-    const int bp = (k - 1) & (NB - 1);
+    bk = k & (NB - 1);
+    bp = (k - 1) & (NB - 1);
     E nw[CY][CX];  // newest plane of the level below (produced this advance)
     {
       const uint32_t pos = ring_cnt + (uint32_t)(k - ka);
@@ -745,6 +921,10 @@ __device__ __forceinline__ int stream3d_unit_pm(const CUtensorMap* tm, E* __rest
       const int q = k - 2 * s;  // target completed this advance (= consumed plane - 1)
       bool fpl = false;
       if constexpr (FPL) fpl = (q < 1) || (q >= n0 - 1);
+      if constexpr (RA) {
+        ra_level(std::integral_constant<int, s>{}, q, fpl, nw);
+        return;
+      }
       // gather the consumed plane (level s-1, produced last advance) once
       E e[CY + 2][CX + 2];
 #pragma unroll

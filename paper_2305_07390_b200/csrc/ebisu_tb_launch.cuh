@@ -79,6 +79,16 @@ constexpr int s2d_minb(int T, int R, int C, int NW, int ebytes = 8) {
         0, (int)sizeof(E)                                                                     \
   }
 
+// explicit MINB (CTAs per SM the register budget targets)
+#define EBISU_S2D_ENTRY_M(SHAPE_ID, SH, T, C, NW, S, EX, UNI, E, SHIFT, MINB)                  \
+  TbKernel {                                                                                  \
+    SHAPE_ID, 2, T, C, NW, S, EX, UNI, Stream2DCfg<SH, T, C, NW, S, E>::SMEM_BYTES, 32 * C, 1, \
+        1, Stream2DCfg<SH, T, C, NW, S, E>::VW, 0, 0, 0,                                     \
+        (const void*)&k_stream2d<SH, T, C, NW, S, (EX) != 0, (UNI) != 0, MINB, E, SHIFT>,     \
+        &launch_stream2d<SH, T, C, NW, S, (EX) != 0, (UNI) != 0, MINB, E, SHIFT>, 0,          \
+        (int)sizeof(E)                                                                        \
+  }
+
 template <class SH, int T, int CY, int CX, int NWY, int S, int FL, bool EXACT, bool UNI, int MINB,
           class E>
 cudaError_t launch_stream3d(const TbLaunch& L) {

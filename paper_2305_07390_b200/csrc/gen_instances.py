@@ -29,6 +29,20 @@ SHIFT_2D = {"j2ds25pt": [(1, 4, 4), (2, 4, 4)]}  # (t, C, U): U=4 251, U=1 240, 
 # (R = 3 with U = 4 shifted windows measured 480 / 531 vs rotating 530 / 552: rotating)
 SHIFT_2D_AFTER = {}  # shifted variants registered after the rotating kernels
 
+# tolerance-mode (exact = 0) kernels for uniform coefficients: reassociated
+# tap sums (stream2d_unit's block_ra, shifted windows of 4 rows, 4 cells per
+# lane): (T, MINB, SHIFT, S) -- SHIFT 4: level-major shifted windows (shared
+# column sums of 4 targets, large radii), 0: rotating windows
+RA_2D = {"j2ds25pt": [(1, 2, 4, 16)],
+         "j2d13pt": [(2, 2, 0, 8), (1, 2, 4, 16), (3, 2, 0, 8)],
+         "j2d25pt": [(3, 2, 0, 8), (1, 2, 0, 16), (2, 2, 0, 8)],
+         "j2d9pt_gol": [(6, 2, 0, 8), (1, 2, 0, 16), (2, 2, 0, 8), (3, 2, 0, 8), (4, 2, 0, 8)],
+         "j2d9pt": [(3, 2, 0, 8), (1, 2, 0, 16), (2, 2, 0, 8)]}
+
+# tolerance-mode halo-exchange kernels (halo2d_unit's block_ra, stars with
+# R >= 4): (T, C, MINB, S)
+RA_H2D = {"j2ds25pt": [(1, 4, 1, 16), (2, 2, 1, 16)]}
+
 # 3-D: shape id, C++ type, tag, list of (T, CY, CX, NWY, S, DEC, MINB); the first
 # entry per depth is the planner default.
 S3D = [
@@ -46,6 +60,12 @@ S3D = [
     ("SHAPE_J3D17PT", "NoCornerShape3<true>", "j3d17pt", [(1, 4, 2, 8, 4, 0, 1), (2, 4, 2, 8, 4, 0, 1)]),
     ("SHAPE_POISSON", "NoCornerShape3<false>", "poisson", [(1, 4, 2, 8, 4, 0, 1), (2, 4, 2, 8, 4, 0, 1)]),
 ]
+
+# tolerance-mode (exact = 0) kernels for uniform coefficients: reassociated
+# tap sums (stream3d_unit_pm's pattern sums), same tile configs as "u"
+RA_3D = {"j3d27pt": [(2, 4, 2, 8, 4, 0, 1), (1, 4, 2, 8, 4, 0, 1)],
+         "poisson": [(2, 4, 2, 8, 4, 0, 1), (1, 4, 2, 8, 4, 0, 1)],
+         "j3d17pt": [(2, 4, 2, 8, 4, 0, 1), (1, 4, 2, 8, 4, 0, 1)]}
 
 # 2-CTA cluster kernels (ebisu_stream3d_cl.cuh: one 64x64 tile over two SMs,
 # DSMEM seam exchange), shared-product fp64: (T, CY, CX, NWY, S); registered
@@ -175,6 +195,30 @@ def main():
                             f"1, 1),\n" for t, cy, cx, nwy, ss in CL3D[tag]]
             _write_tu(arr, f"ebisu_inst_{tag}_{kind}.cu", tag, sh, entries)
             units.append(arr)
+    for sid, sh, tag, _ in S2D:
+        if tag not in RA_2D:
+            continue
+        arr = f"k_{tag}_r"
+        entries = [f"    EBISU_S2D_ENTRY_M({sid}, SH_{tag}, {t}, 4, {NW}, {ss}, 0, 1, double, {u}, {mb}),\n"
+                   for t, mb, u, ss in RA_2D[tag]]
+        _write_tu(arr, f"ebisu_inst_{tag}_r.cu", tag, sh, entries)
+        units.append(arr)
+    for sid, sh, tag, _ in H2D:
+        if tag not in RA_H2D:
+            continue
+        arr = f"k_h2d_{tag}_r"
+        entries = [f"    EBISU_H2D_ENTRY_SH({sid}, SH_{tag}, {t}, {c}, {H2D_NW}, {ss}, 0, 1, {mb}, 4),\n"
+                   for t, c, mb, ss in RA_H2D[tag]]
+        _write_tu(arr, f"ebisu_inst_h2d_{tag}_r.cu", tag, sh, entries)
+        units.append(arr)
+    for sid, sh, tag, _ in S3D:
+        if tag not in RA_3D:
+            continue
+        arr = f"k_{tag}_r"
+        entries = [f"    EBISU_S3D_ENTRY({sid}, SH_{tag}, {t}, {cy}, {cx}, {nwy}, {ss}, "
+                   f"{dec}, 0, 1, {mb}, double),\n" for t, cy, cx, nwy, ss, dec, mb in RA_3D[tag]]
+        _write_tu(arr, f"ebisu_inst_{tag}_r.cu", tag, sh, entries)
+        units.append(arr)
     for sid, sh, tag, _ in S2D:
         arr = f"k_{tag}_s"
         entries = [f"    EBISU_S2D_ENTRY({sid}, SH_{tag}, {t}, {c}, {NW}, {S}, 1, 1, float),\n"

@@ -93,6 +93,7 @@ def sweep_device(d_in, stencil: StencilShape, steps: int, *, out=None, scratch=N
     if trace:
         d = tr.to_dict()
         d["kernel"] = _native.kernel_name(tr.kernel_id)
+        d["arith"] = _native.ARITH_NAMES.get(tr.arith, str(tr.arith))
         return out, d
     return out
 

@@ -125,6 +125,7 @@ def sweep(grid: Grid, stencil: StencilShape, steps: int, *, t: int = 0,
     if trace:
         d = tr.to_dict()
         d["kernel"] = _native.kernel_name(tr.kernel_id)
+        d["arith"] = _native.ARITH_NAMES.get(tr.arith, str(tr.arith))
         return out, d
     return out
 

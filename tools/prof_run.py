@@ -12,8 +12,10 @@ out = torch.empty_like(d_in); scr = torch.empty_like(d_in)
 scheme = int(sys.argv[6]) if len(sys.argv) > 6 else 0
 # EBISU_PERSISTENT=0: one launch per epoch (ncu cannot replay a cooperative
 # cluster launch)
+# EBISU_EXACT=0: tolerance mode (reassociated kernels for uniform coefficients)
 prm = _native.make_params(scheme=scheme, t=t, variant=var,
-                          persistent=os.environ.get("EBISU_PERSISTENT", "1") != "0")
+                          persistent=os.environ.get("EBISU_PERSISTENT", "1") != "0",
+                          exact=os.environ.get("EBISU_EXACT", "1") != "0")
 for _ in range(2):
     _, tr = device.sweep_device(d_in, st, steps, out=out, scratch=scr, params=prm, trace=True)
 print(tr)

@@ -48,7 +48,7 @@ class _Trace(ctypes.Structure):  # ebisu_trace
         "syncs_device", "cells_computed", "cells_valid", "device_tiles",
         "kernel_launches")] + [("elapsed_ms", ctypes.c_double)] + [
         (n, ctypes.c_int32) for n in ("kernel_id", "t_used", "grid_ctas",
-                                      "warps_per_cta")] + [("reserved", ctypes.c_int32 * 4)]
+                                      "warps_per_cta", "arith")] + [("reserved", ctypes.c_int32 * 3)]
 
 
 _lib = ctypes.CDLL(_LIB)
