@@ -76,7 +76,11 @@ typedef enum ebisu_scheme {
   EBISU_SCHEME_AUTO = 0,          /* planner picks (temporal blocking when possible) */
   EBISU_SCHEME_NAIVE = 1,         /* one sm_100a launch per time step (yardstick)    */
   EBISU_SCHEME_SM_TILING = 2,     /* overlapped streaming tiles, "sm-tiling"        */
-  EBISU_SCHEME_DEVICE_TILING = 3  /* halo-exchange tiles, "device-tiling"           */
+  EBISU_SCHEME_DEVICE_TILING = 3, /* halo-exchange tiles, "device-tiling"           */
+  EBISU_SCHEME_RESIDENT = 4       /* resident tiles, runtime taps: any stencil (AUTO
+                                     uses it for shapes without a specialised kernel,
+                                     e.g. 1-D and user tap sets, when the cost model
+                                     beats one launch per step)                      */
 } ebisu_scheme;
 
 /* Stencil shape: reference StencilShape (shapes.py:27-56).  offsets holds
@@ -144,7 +148,8 @@ typedef struct ebisu_trace {
   int32_t grid_ctas;
   int32_t warps_per_cta;
   int32_t arith;             /* EBISU_ARITH_*: arithmetic of the main stage        */
-  int32_t reserved[3];
+  int32_t cluster_ctas;      /* CTAs per cluster tile (device tile) of the main stage */
+  int32_t reserved[2];
 } ebisu_trace;
 
 /* ebisu_trace.arith */

@@ -28,6 +28,7 @@ SCHEME_AUTO = 0
 SCHEME_NAIVE = 1
 SCHEME_SM_TILING = 2
 SCHEME_DEVICE_TILING = 3
+SCHEME_RESIDENT = 4  # resident tiles, runtime taps (any stencil)
 
 # Every symbol include/ebisu.h declares (checked by tests/test_native_abi.py).
 ABI_VERSION = 2  # include/ebisu.h EBISU_ABI_VERSION (ParamsC layout below)
@@ -102,7 +103,8 @@ class TraceC(ctypes.Structure):
         ("grid_ctas", ctypes.c_int32),
         ("warps_per_cta", ctypes.c_int32),
         ("arith", ctypes.c_int32),
-        ("reserved", ctypes.c_int32 * 3),
+        ("cluster_ctas", ctypes.c_int32),
+        ("reserved", ctypes.c_int32 * 2),
     ]
 
     def to_dict(self) -> dict:

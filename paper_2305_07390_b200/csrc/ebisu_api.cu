@@ -13,6 +13,7 @@
 #include <stdlib.h>
 
 #include <algorithm>
+#include <cmath>
 #include <mutex>
 #include <string>
 #include <vector>
@@ -118,7 +119,7 @@ int validate(const ebisu_stencil* st, int ndim, const int64_t* ext, const ebisu_
   out->coeffs = st->coeffs;
   out->shape_id = identify_shape(st);
   if (prm) {
-    if (prm->scheme < EBISU_SCHEME_AUTO || prm->scheme > EBISU_SCHEME_DEVICE_TILING)
+    if (prm->scheme < EBISU_SCHEME_AUTO || prm->scheme > EBISU_SCHEME_RESIDENT)
       return fail(EBISU_ERR_PARAM, "unknown scheme %d", prm->scheme);
     if (prm->t < 0) return fail(EBISU_ERR_PARAM, "temporal depth must be >= 1");
     if (prm->out_planes[1] != 0 &&
@@ -246,6 +247,7 @@ enum KernelId : int {
   KID_STREAM2D = 2,
   KID_STREAM3D = 3,
   KID_HALO2D = 4,
+  KID_GENERIC = 5,
 };
 
 // First registered kernel for (shape, depth, exactness) -- the registry lists
@@ -340,12 +342,14 @@ struct Stage {
   int kind;            // KID_*
   const TbKernel* k;   // for TB stages
   int epochs;          // fused epochs (TB) or steps (naive)
+  int T = 0;           // KID_GENERIC: levels per epoch
 };
 
 struct Counters {
   uint64_t gm_loads = 0, gm_stores = 0, cells_computed = 0, device_tiles = 0, syncs_device = 0,
            syncs_block = 0, launches = 0, halo_loads = 0, halo_stores = 0;
   int grid = 0, nw = 0, t_used = 0, kid = KID_NONE;
+  int cluster = 1;  // CTAs per cluster tile of the main stage
   int arith = -1;  // EBISU_ARITH_* of the first (main) stage
 };
 
@@ -554,7 +558,8 @@ int run_tb2d_stage(const ProblemDesc& p, const TbKernel* k, int epochs, int firs
 
 int run_halo2d_stage(const ProblemDesc& p, const TbKernel* k, int epochs, int first_src,
                      int first_dst, void* bufs[3], const CUtensorMap maps[3], bool coop_req,
-                     int seg_rows_req, const DevInfo& di, cudaStream_t st, Counters* ctr) {
+                     int seg_rows_req, int cl_req, const DevInfo& di, cudaStream_t st,
+                     Counters* ctr) {
   const int n0 = (int)p.ext[0], n1 = (int)p.ext[1];
   const int T = k->T, R = p.rad;
   int per_sm = 0;
@@ -563,28 +568,80 @@ int run_halo2d_stage(const ProblemDesc& p, const TbKernel* k, int epochs, int fi
   EB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k->func, k->NW * 32,
                                                         (size_t)k->smem_bytes));
   if (per_sm < 1) return fail(EBISU_ERR_CUDA, "halo2d kernel cannot be resident (T=%d)", T);
-  const int max_ctas = per_sm * di.sms;
   const int LW = k->wn, VW = k->valid_x, HX = (LW - VW) / 2, Z = k->z;
-  // edge-aligned strips when two fit (frame columns then sit in the first /
-  // last strip only); generic strips otherwise
-  int aligned = n1 >= 2 * LW ? 1 : 0;
-  int nstrips;
-  if (aligned) {
-    const int mid = strip_last_x0(n1, LW, 2) - VW;
-    nstrips = 2 + (mid > 0 ? (mid + VW - 1) / VW : 0);
-  } else {
-    nstrips = (n1 + VW - 1) / VW;
+  // Device tile = a cluster of CL CTA strips side by side (the reference's
+  // device_tile_grid, engine/device.py:91-93): only the tile's outer edges
+  // carry the t*R margin, the CL-1 seams exchange edges through DSMEM.  One
+  // tile spanning the whole width has no margin at all.
+  auto strips_for = [&](int cl, int* aligned) {
+    const int LWc = cl * LW, VWc = LWc - 2 * HX;
+    if (LWc >= n1) {
+      *aligned = 0;
+      return 1;
+    }
+    *aligned = n1 >= 2 * LWc ? 1 : 0;
+    if (*aligned) {
+      const int mid = strip_last_x0(n1, LWc, 2) - VWc;
+      return 2 + (mid > 0 ? (mid + VWc - 1) / VWc : 0);
+    }
+    return (n1 + VWc - 1) / VWc;
+  };
+  // reassociated (tolerance) kernels exchange once per block of advances:
+  // single-CTA tiles only
+  const bool ra = k->uni && !k->exact;
+  // the cluster-tile twin of this kernel (same shape, depth, lanes, arithmetic)
+  const TbKernel* kc = nullptr;
+  if (!ra) {
+    int nk = 0;
+    const TbKernel* ks = tb_kernels(&nk);
+    for (int i = 0; i < nk && !kc; ++i)
+      if (ks[i].max_clusters_n && ks[i].shape_id == k->shape_id && ks[i].T == T &&
+          ks[i].C == k->C && ks[i].exact == k->exact && ks[i].uni == k->uni &&
+          ks[i].elem == k->elem && ks[i].family == 1)
+        kc = &ks[i];
   }
+  int cl = 1, max_ctas = per_sm * di.sms;
+  if (cl_req > 1 && !kc)
+    return fail(EBISU_ERR_UNSUPPORTED,
+                "no cluster-tile halo-exchange kernel for this stencil at depth %d", T);
+  if (kc) {
+    double best = -1;
+    const int cands[4] = {1, 2, 4, 8};
+    for (int c : cands) {
+      if (cl_req > 0 && c != std::min(cl_req, 8)) continue;
+      int slots = per_sm * di.sms;
+      if (c > 1) {
+        int ncl = 0;
+        EB_CUDA(kc->max_clusters_n(c, &ncl));
+        slots = ncl * c;
+      }
+      if (slots < c) continue;
+      int al = 0;
+      // CTA strips of work per row over the resident CTAs (lower is better)
+      const double cost = (double)strips_for(c, &al) * c / slots;
+      if (best < 0 || cost < best * 0.99) {
+        best = cost;
+        cl = c;
+        max_ctas = slots;
+      }
+    }
+    if (best < 0)
+      return fail(EBISU_ERR_UNSUPPORTED, "no resident cluster of %d halo-exchange CTAs", cl_req);
+    if (cl > 1) k = kc;
+  }
+  int aligned = 0;
+  const int nstrips = strips_for(cl, &aligned);
   const int span = p.z_hi - p.z_lo;
   int nseg = 1, seg_len = span;
-  plan_segments(span, nstrips, max_ctas, T * (R + Z), std::max(16, 2 * T * Z), &nseg, &seg_len);
+  plan_segments(span, nstrips, max_ctas / cl, T * (R + Z), std::max(16, 2 * T * Z), &nseg,
+                &seg_len);
   if (seg_rows_req > 0) {
     seg_len = seg_rows_req;
     nseg = (span + seg_len - 1) / seg_len;
   }
   const long long units = (long long)nstrips * nseg;
-  int grid = (int)std::min<long long>(max_ctas, units);
-  if (grid < 1) grid = 1;
+  int grid = (int)std::min<long long>(max_ctas / cl, units) * cl;
+  if (grid < cl) grid = cl;
   const bool coop = coop_req && di.coop && epochs > 1;
   TbLaunch L{};
   L.n0 = n0;
@@ -601,6 +658,7 @@ int run_halo2d_stage(const ProblemDesc& p, const TbKernel* k, int epochs, int fi
   L.coeffs = p.coeffs;
   L.grid = grid;
   L.stream = st;
+  L.cluster = cl;
   int* work = nullptr;
   if (int rc = alloc_work(epochs, st, &work)) return rc;
   if (coop) {
@@ -628,7 +686,8 @@ int run_halo2d_stage(const ProblemDesc& p, const TbKernel* k, int epochs, int fi
   }
   cudaFreeAsync(work, st);
   // closed-form counters: every advance loads one row per warp; halo traffic
-  // = 2R edge values per produced row per warp and level (shared memory)
+  // = 2R edge values per produced row per warp and level (shared memory and,
+  // across the cluster seams, DSMEM)
   uint64_t adv = 0;
   const int Wr = Z + R + 1;
   for (int g = 0; g < nseg; ++g) {
@@ -636,15 +695,17 @@ int run_halo2d_stage(const ProblemDesc& p, const TbKernel* k, int epochs, int fi
     const int ka = std::max(0, r0 - T * R);
     adv += (uint64_t)((r1 + T * Z - ka + Wr - 1) / Wr * Wr);
   }
-  ctr->gm_loads += (uint64_t)epochs * adv * (uint64_t)LW * (uint64_t)nstrips;
+  const uint64_t cols = (uint64_t)LW * cl * nstrips;
+  ctr->gm_loads += (uint64_t)epochs * adv * cols;
   ctr->gm_stores += (uint64_t)epochs * (uint64_t)span * (uint64_t)n1;
-  ctr->cells_computed += (uint64_t)epochs * adv * (uint64_t)T * (uint64_t)LW * (uint64_t)nstrips;
-  ctr->halo_stores += (uint64_t)epochs * adv * (uint64_t)T * 2ull * R * k->NW * nstrips;
-  ctr->halo_loads += (uint64_t)epochs * adv * (uint64_t)T * 2ull * R * k->NW * nstrips;
-  ctr->syncs_block += (uint64_t)epochs * adv * (uint64_t)nstrips;
+  ctr->cells_computed += (uint64_t)epochs * adv * (uint64_t)T * cols;
+  ctr->halo_stores += (uint64_t)epochs * adv * (uint64_t)T * 2ull * R * k->NW * cl * nstrips;
+  ctr->halo_loads += (uint64_t)epochs * adv * (uint64_t)T * 2ull * R * k->NW * cl * nstrips;
+  ctr->syncs_block += (uint64_t)epochs * adv * (uint64_t)nstrips * cl;
   ctr->device_tiles += (uint64_t)epochs * (uint64_t)units;
   ctr->grid = grid;
   ctr->nw = k->NW;
+  ctr->cluster = cl;
   ctr->t_used = std::max(ctr->t_used, T);
   if (ctr->arith < 0) ctr->arith = arith_of(k);
   if (ctr->kid == KID_NONE) ctr->kid = KID_HALO2D;
@@ -768,6 +829,213 @@ int run_tb3d_stage(const ProblemDesc& p, const TbKernel* k, int epochs, int firs
   return EBISU_OK;
 }
 
+// ---- resident-tile kernel (any tap set): tile shape and depth ----------------
+// Tile-shape cost model in SM clocks (the grid's tiles spread over all SMs):
+//   compute  per level: the level's region x (ntaps loads + 1 store) x elem /
+//            128 B/clk of shared memory / kSmemEff, plus kLevelLatency
+//   HBM      (loaded + core) x elem / kHbmBytesPerClkSm + kTileLatency,
+//            overlapped with the other CTA's compute at 2 CTAs per SM
+// (B200: 7.7 TB/s / 148 SMs / 1.9 GHz ~ 27 B/clk; 23 sustained.)
+constexpr double kHbmBytesPerClkSm = 23.0;
+constexpr double kSmemEff = 0.45;      // measured share of the shared-memory rate
+constexpr double kTileLatency = 2500;  // clocks: tile load round trip + store drain
+constexpr double kLevelLatency = 300;  // clocks: per-level barrier and pipeline drain
+constexpr int kGenSmemBytes = 227 * 1024;
+
+// resident CTAs per SM (EBISU_GEN_CTAS, measurement knob): 1 = one 227 KB
+// tile per SM, 2 = two half-size tiles whose load and compute phases overlap
+int gen_ctas_per_sm() {
+  static const int v = [] {
+    const char* e = getenv("EBISU_GEN_CTAS");
+    const int n = e ? atoi(e) : 2;
+    return n == 1 ? 1 : 2;
+  }();
+  return v;
+}
+
+struct GenPlan {
+  GenArgs a;
+  double clk_per_cell_step;  // whole-GPU estimate (all SMs)
+  int grid;
+  int smem;
+  int threads;
+};
+
+bool gen_plan(const ProblemDesc& p, int T, int sms, GenPlan* out) {
+  const int D = p.dims, R = p.rad;
+  GenArgs a;
+  memset(&a, 0, sizeof(a));
+  for (int ax = 0; ax < 3; ++ax) a.ext[ax] = 1;
+  for (int d = 0; d < D; ++d) a.ext[3 - D + d] = p.ext[d];
+  a.pitch = p.pitch ? p.pitch : p.ext[D - 1];
+  a.zaxis = 3 - D;
+  a.z_lo = p.z_lo;
+  a.z_hi = p.z_hi;
+  a.T = T;
+  long long span[3];
+  for (int ax = 0; ax < 3; ++ax) {
+    const bool present = ax >= 3 - D;
+    a.H[ax] = present ? T * R : 0;
+    a.RA[ax] = present ? R : 0;
+    a.F[ax] = present ? R : 0;
+    span[ax] = ax == a.zaxis ? (long long)(p.z_hi - p.z_lo) : a.ext[ax];
+  }
+  // per-CTA budget: 228 KB per SM less 1 KB reserved per resident CTA
+  const long long budget = std::min(kGenSmemBytes, 228 * 1024 / gen_ctas_per_sm() - 1024);
+  const long long cap = budget / (2 * p.elem) - 128;  // + 128 pad elements per buffer
+  static const int cand[] = {16, 24, 32, 48, 64, 96, 128, 160, 192, 256, 320, 384, 512,
+                             768, 1024, 1536, 2048, 4096, 8192, 16384, 32768};
+  // candidate extents of one axis: the list plus "whole span", <= limit
+  auto axis_cands = [&](int ax, long long limit, std::vector<int>& v) {
+    v.clear();
+    const long long whole = span[ax] + 2LL * a.H[ax];
+    for (int c : cand)
+      if (c > 2 * a.H[ax] && c < whole && c <= limit) v.push_back(c);
+    if (whole <= limit) v.push_back((int)whole);
+    if (v.empty() && limit > 2 * a.H[ax] && limit < whole) v.push_back((int)limit);
+  };
+  // measured: the kernel sustains ~45 % of the shared-memory rate (1-D j1d3pt
+  // t=16 499 GCells/s, 2-D j2d5pt-order-reversed t=8 273 GCells/s)
+  const double per_cell_smem = (double)(p.ntaps + 1) * p.elem / 128.0 / kSmemEff;
+  double best = 1e300;
+  GenArgs bestA = a;
+  std::vector<int> c2, c1, c0;
+  axis_cands(2, cap, c2);
+  for (int L2 : c2) {
+    axis_cands(1, cap / L2, c1);
+    if (D < 2) c1.assign(1, 1);
+    for (int L1 : c1) {
+      if ((long long)L1 * L2 > cap) continue;
+      long long lim0 = cap / ((long long)L1 * L2);
+      int L0;
+      if (D < 3) {
+        L0 = 1;
+      } else {
+        L0 = (int)std::min<long long>(lim0, span[0] + 2LL * a.H[0]);
+        if (L0 <= 2 * a.H[0]) continue;
+      }
+      const int L[3] = {L0, L1, L2};
+      int V[3];
+      long long nt[3];
+      bool ok = true;
+      for (int ax = 0; ax < 3; ++ax) {
+        V[ax] = L[ax] - 2 * a.H[ax];
+        if (V[ax] <= 0) ok = false;
+        nt[ax] = ok ? (span[ax] + V[ax] - 1) / V[ax] : 0;
+      }
+      if (!ok) continue;
+      double comp = 0;
+      for (int s = 1; s <= T; ++s) {
+        const long long w0 = L0 - 2LL * s * a.RA[0], w1 = L1 - 2LL * s * a.RA[1];
+        const long long w2 = L2 - 2LL * s * a.RA[2];
+        comp += (double)(w0 * w1) * (double)((w2 + 127) / 128 * 128) * per_cell_smem;
+      }
+      const double cells_l = (double)L0 * L1 * L2, cells_v = (double)V[0] * V[1] * V[2];
+      // HBM bytes plus the exposed load round trip (~kTileLatency clocks)
+      const double mem = (cells_l + cells_v) * p.elem / kHbmBytesPerClkSm + kTileLatency;
+      comp += T * kLevelLatency;  // barrier + pipeline drain per level
+      const long long ntiles = nt[0] * nt[1] * nt[2];
+      if (ntiles > (1LL << 31)) continue;
+      const int cps = gen_ctas_per_sm();
+      const double waves = std::ceil((double)ntiles / (sms * cps)) * cps;
+      // two CTAs per SM overlap one tile's HBM phase with the other's compute
+      const double total = cps > 1 ? waves / cps * std::max(2 * comp, comp + mem)
+                                   : waves * (comp + mem);
+      const double cells = (double)span[0] * span[1] * span[2] * T;
+      const double cost = total / cells;
+      if (cost < best) {
+        best = cost;
+        for (int ax = 0; ax < 3; ++ax) {
+          bestA.L[ax] = L[ax];
+          bestA.V[ax] = V[ax];
+          bestA.nt[ax] = (int)nt[ax];
+        }
+      }
+    }
+  }
+  if (best >= 1e300) return false;
+  a = bestA;
+  a.ntaps = p.ntaps;
+  for (int k = 0; k < p.ntaps; ++k) {
+    const int* o = p.offsets + k * D;
+    int off[3] = {0, 0, 0};
+    for (int d = 0; d < D; ++d) off[3 - D + d] = o[d];
+    a.lin[k] = (off[0] * a.L[1] + off[1]) * a.L[2] + off[2];
+    a.coef[k] = p.coeffs[k];
+  }
+  out->a = a;
+  out->clk_per_cell_step = best;
+  const long long ntiles = (long long)a.nt[0] * a.nt[1] * a.nt[2];
+  out->grid = (int)std::min<long long>(ntiles, (long long)sms * gen_ctas_per_sm());
+  out->smem = 2 * (a.L[0] * a.L[1] * a.L[2] + 128) * p.elem;  // kGenPad per buffer
+  out->threads = generic_threads() / gen_ctas_per_sm();
+  return true;
+}
+
+// Depth for the resident-tile kernel: the requested one (else the deepest
+// below it that fits); AUTO uses the kernel only where it measured faster than
+// one launch per step.  Measured on B200 (tools/gen_bench.py, 64 steps):
+//   1-D j1d3pt 2^25 cells   resident t=16 539 GCells/s vs naive 364
+//   2-D 8192^2, 5/9/13 taps resident t=8 273/208/131 vs naive 338/287/215
+//   3-D 512^3, 7/27 taps    resident t=2 84/50 vs naive 182/84
+// (the kernel sustains ~45 % of the shared-memory rate with runtime taps:
+// no register reuse between taps).  Forced (scheme RESIDENT) without a depth:
+// the measured-best depth per dimensionality.
+int gen_pick_depth(const ProblemDesc& p, int t_req, int sms, bool forced) {
+  int want = t_req;
+  if (want <= 0) {
+    if (p.dims == 1)
+      want = 16;
+    else if (forced)
+      want = p.dims == 2 ? 8 : 2;
+    else
+      return 0;
+  }
+  for (int T = want; T >= 1; --T) {
+    GenPlan g;
+    if (gen_plan(p, T, sms, &g)) return T;
+  }
+  return 0;
+}
+
+int run_generic_stage(const ProblemDesc& p, int T, int epochs, int first_src, int first_dst,
+                      void* bufs[3], bool exact, const DevInfo& di, cudaStream_t st,
+                      Counters* ctr) {
+  GenPlan g;
+  if (!gen_plan(p, T, di.sms, &g))
+    return fail(EBISU_ERR_UNSUPPORTED, "no resident tile fits depth %d at radius %d", T, p.rad);
+  int src = first_src, dst = first_dst;
+  for (int e = 0; e < epochs; ++e) {
+    g.a.in = bufs[src];
+    g.a.out = bufs[dst];
+    EB_CUDA(launch_generic_tb(g.a, p.elem, exact, g.grid, g.threads, g.smem, st));
+    ctr->launches += 1;
+    src = dst;
+    dst = (dst == BUF_OUT) ? BUF_SCR : BUF_OUT;
+  }
+  // closed-form counters
+  const GenArgs& a = g.a;
+  const uint64_t ntiles = (uint64_t)a.nt[0] * a.nt[1] * a.nt[2];
+  uint64_t comp = 0;
+  for (int s = 1; s <= T; ++s)
+    comp += (uint64_t)(a.L[0] - 2 * s * a.RA[0]) * (uint64_t)(a.L[1] - 2 * s * a.RA[1]) *
+            (uint64_t)(a.L[2] - 2 * s * a.RA[2]);
+  uint64_t span = 1;
+  for (int ax = 0; ax < 3; ++ax)
+    span *= (uint64_t)(ax == a.zaxis ? (a.z_hi - a.z_lo) : a.ext[ax]);
+  ctr->gm_loads += (uint64_t)epochs * ntiles * (uint64_t)a.L[0] * a.L[1] * a.L[2];
+  ctr->gm_stores += (uint64_t)epochs * span;
+  ctr->cells_computed += (uint64_t)epochs * ntiles * comp;
+  ctr->device_tiles += (uint64_t)epochs * ntiles;
+  ctr->syncs_block += (uint64_t)epochs * ntiles * (uint64_t)(T + 2);
+  ctr->grid = g.grid;
+  ctr->nw = g.threads / 32;
+  ctr->t_used = std::max(ctr->t_used, T);
+  if (ctr->arith < 0) ctr->arith = exact ? EBISU_ARITH_PER_TAP_EXACT : EBISU_ARITH_PER_TAP_FMA;
+  if (ctr->kid == KID_NONE) ctr->kid = KID_GENERIC;
+  return EBISU_OK;
+}
+
 int run_device_impl(const ProblemDesc& p0, const void* d_in, void* d_out, void* d_scr,
                     long long steps, const ebisu_params* prm, cudaStream_t st, Counters* ctr) {
   ProblemDesc p = p0;
@@ -796,8 +1064,9 @@ int run_device_impl(const ProblemDesc& p0, const void* d_in, void* d_out, void* 
   // (pitch rounded up to 16 bytes; TMA maps keep the true extent, so the pad
   // is never read): one strided copy in, one out -- two grid passes per sweep
   // instead of falling back to one-launch-per-step.
+  const bool force_gen = scheme == EBISU_SCHEME_RESIDENT;
   const bool tb_shape = (D == 2 || D == 3) && p.shape_id != SHAPE_GENERIC &&
-                        scheme != EBISU_SCHEME_NAIVE;
+                        scheme != EBISU_SCHEME_NAIVE && !force_gen;
   const bool tma_direct = ((p.ext[D - 1] * p.elem) % 16 == 0) &&
                           (reinterpret_cast<uintptr_t>(d_in) % 16 == 0) &&
                           (reinterpret_cast<uintptr_t>(d_out) % 16 == 0) &&
@@ -856,9 +1125,20 @@ int run_device_impl(const ProblemDesc& p0, const void* d_in, void* d_out, void* 
   if (pitched)
     for (auto& s : stages) tb_ok = tb_ok && s.kind != KID_NAIVE;
   if (!tb_ok) {
+    // no specialised kernel (1-D, user tap sets, or forced): the resident-tile
+    // kernel for any tap set when its cost model beats one launch per step
     pitched = false;
     stages.clear();
-    stages.push_back({KID_NAIVE, nullptr, (int)steps});
+    const int tg = scheme == EBISU_SCHEME_NAIVE
+                       ? 0
+                       : gen_pick_depth(p, (prm && prm->t > 0) ? prm->t : 0, di.sms, force_gen);
+    if (tg > 0) {
+      const long long full = steps / tg, rem = steps % tg;
+      if (full > 0) stages.push_back({KID_GENERIC, nullptr, (int)full, tg});
+      if (rem > 0) stages.push_back({KID_GENERIC, nullptr, 1, (int)rem});
+    } else {
+      stages.push_back({KID_NAIVE, nullptr, (int)steps});
+    }
   }
 
   // ---- buffers: every stage writes a full grid (frame included) -----------------
@@ -951,6 +1231,10 @@ int run_device_impl(const ProblemDesc& p0, const void* d_in, void* d_out, void* 
       if (ctr->kid == KID_NONE) ctr->kid = KID_NAIVE;
       ctr->t_used = std::max(ctr->t_used, 1);
       src = (s.epochs % 2 == 1) ? dst : (dst == BUF_OUT ? BUF_SCR : BUF_OUT);
+    } else if (s.kind == KID_GENERIC) {
+      result = run_generic_stage(p, s.T, s.epochs, src, dst, bufs, exact, di, st, ctr);
+      if (result) break;
+      src = (s.epochs % 2 == 1) ? dst : (dst == BUF_OUT ? BUF_SCR : BUF_OUT);
     } else {
       {
         // 2-D: one 32*C-column row per TMA box; 3-D: one LY x LX tile plane
@@ -968,7 +1252,8 @@ int run_device_impl(const ProblemDesc& p0, const void* d_in, void* d_out, void* 
       }
       if (D == 2 && s.kind == KID_HALO2D)
         result = run_halo2d_stage(p, s.k, s.epochs, src, dst, bufs, maps, coop,
-                                  prm ? prm->seg_rows : 0, di, st, ctr);
+                                  prm ? prm->seg_rows : 0, prm ? prm->device_tile_grid[1] : 0,
+                                  di, st, ctr);
       else if (D == 2)
         result = run_tb2d_stage(p, s.k, s.epochs, src, dst, bufs, maps, coop,
                                 prm ? prm->seg_rows : 0, di, st, ctr);
@@ -1011,6 +1296,7 @@ const char* ebisu_kernel_name(int32_t id) {
     case KID_STREAM2D: return "stream2d_tb";
     case KID_STREAM3D: return "stream3d_tb";
     case KID_HALO2D: return "halo2d_tb";
+    case KID_GENERIC: return "resident_tb";
     default: return "none";
   }
 }
@@ -1052,6 +1338,7 @@ static void fill_trace(ebisu_trace* tr, const ProblemDesc& p, long long steps, c
   tr->t_used = c.t_used;
   tr->grid_ctas = c.grid;
   tr->warps_per_cta = c.nw;
+  tr->cluster_ctas = c.cluster;
   tr->arith = c.arith < 0 ? EBISU_ARITH_SHARED_PRODUCTS : c.arith;
 }
 

@@ -60,8 +60,15 @@ struct Halo2DCfg {
   static constexpr int NB = NBMIN <= 2 ? 2 : (NBMIN <= 4 ? 4 : (NBMIN <= 8 ? 8 : 16));
   static constexpr int ROW_BYTES = LC * 8;
   static constexpr int RING_BYTES = NW * S * ROW_BYTES;
-  static constexpr int XH_DOUBLES = T * NB * NW * 2 * R;  // levels 0..T-1
-  static constexpr int SMEM_BYTES = RING_BYTES + XH_DOUBLES * 8 + (NW * S + DR) * 8;
+  // edge buffer columns: 0 = left neighbour CTA's last warp (cluster),
+  // 1..NW = this CTA's warps, NW+1 = right neighbour CTA's first warp
+  static constexpr int XCOLS = NW + 2;
+  static constexpr int XH_DOUBLES = T * NB * XCOLS * 2 * R;  // levels 0..T-1
+  // mbarriers: TMA ring (NW*S), advance barriers (DR), foreign-edge receive
+  // barriers fullL/fullR and slot-release barriers emptyL/emptyR (NB each),
+  // then the unit id
+  static constexpr int BAR_OFF = RING_BYTES + XH_DOUBLES * 8;
+  static constexpr int SMEM_BYTES = BAR_OFF + (NW * S + DR + 4 * NB) * 8 + 16;
   static_assert(VW > 0, "strip leaves no valid core");
   static_assert(NB >= NBMIN, "edge-buffer slots must cover lag + drift");
   static_assert((S & (S - 1)) == 0, "ring slots must be a power of two");
@@ -82,11 +89,23 @@ struct Halo2DArgs {
   int* work;
 };
 
+// Cluster context of a CTA: rank and size of the device tile (CL CTA strips
+// side by side along axis 1, exchanging their outer warps' edge columns
+// through DSMEM).  Remote addresses are formed on use (mapa): the same
+// shared-memory offsets in the neighbour CTA.
+struct Halo2DCluster {
+  int rank, n;
+  __device__ __forceinline__ bool has_l() const { return rank > 0; }
+  __device__ __forceinline__ bool has_r() const { return rank < n - 1; }
+};
+
 // One unit: CTA strip x row segment.  EDGE: the strip touches a frame column.
-template <class SH, int T, int C, int NW, int S, bool EXACT, bool UNI, bool EDGE, int SHIFT>
+template <class SH, int T, int C, int NW, int S, bool EXACT, bool UNI, bool EDGE, int SHIFT,
+          bool CLU>
 __device__ __forceinline__ int halo2d_unit(const CUtensorMap* tm, double* __restrict__ out,
                                            double* ring, uint64_t* bars, double* xh,
-                                           uint64_t* advbar, uint32_t ring_cnt, uint32_t& adv,
+                                           uint64_t* advbar, const Halo2DCluster& cc,
+                                           uint32_t ring_cnt, uint32_t& adv,
                                            int warp, int lane, int n0, int n1, int pitch, int X0, int vlo,
                                            int vhi, int r0, int r1, const Coefs<SH::NT>& cf) {
   using Cfg = Halo2DCfg<SH, T, C, NW, S>;
@@ -132,30 +151,95 @@ __device__ __forceinline__ int halo2d_unit(const CUtensorMap* tm, double* __rest
       for (int c = 0; c < C; ++c) win[s][w][c] = 0.0;
 
   // edge buffer of (level, slot, warp, side)
+  constexpr int XCOLS = Cfg::XCOLS;
+  uint64_t* const fullL = advbar + Cfg::DR;  // receive barriers (kernel layout)
+  uint64_t* const fullR = fullL + NB;
+  uint64_t* const emptyL = fullR + NB;       // slot releases by the neighbours
+  uint64_t* const emptyR = emptyL + NB;
+  auto xoff = [&](int level, int slot, int w, int side) -> int {
+    return (((level * NB + slot) * XCOLS + w) * 2 + side) * R;
+  };
   auto xrow = [&](int level, int slot, int w, int side) -> double* {
-    return xh + ((size_t)((level * NB + slot) * NW + w) * 2 + side) * R;
+    return xh + xoff(level, slot, w, side);
   };
   // push the warp's leftmost / rightmost R values of a produced row:
   // predicated stores, only the edge lanes' predicates are on (no branch)
   auto push = [&](int level, int slot, const double (&v)[C]) {
-    double* L = xrow(level, slot, warp, 0);
-    double* Rt = xrow(level, slot, warp, 1);
+    double* L = xrow(level, slot, warp + 1, 0);
+    double* Rt = xrow(level, slot, warp + 1, 1);
 #pragma unroll
     for (int c = 0; c < C; ++c) {
       const int col = lane * C + c;
       if (c < R) st_shared_if(L + min(col, R - 1), v[c], col < R);
       if (C - c <= R) st_shared_if(Rt + max(col - (LC - R), 0), v[c], col >= LC - R);
     }
+    // the tile's outer warps also hand their outer edge to the neighbour CTA
+    // of the cluster: st.async into its xh, completing 8 bytes each on its
+    // receive barrier for this advance (no fence: the TMA-style handshake)
+    if (CLU && warp == 0 && cc.has_l() && lane * C < R) {
+      // left CTA: its right-foreign column (NW+1), completing on its fullR
+      const uint32_t dst = mapa_shared(xrow(level, slot, NW + 1, 0), cc.rank - 1);
+      const uint32_t bar = mapa_shared(fullR + slot, cc.rank - 1);
+#pragma unroll
+      for (int c = 0; c < C && c < R; ++c)
+        if (lane * C + c < R) st_async_f64(dst + 8u * (lane * C + c), v[c], bar);
+    }
+    if (CLU && warp == NW - 1 && cc.has_r() && lane * C + C > LC - R) {
+      // right CTA: its left-foreign column (0), completing on its fullL
+      const uint32_t dst = mapa_shared(xrow(level, slot, 0, 1), cc.rank + 1);
+      const uint32_t bar = mapa_shared(fullL + slot, cc.rank + 1);
+#pragma unroll
+      for (int c = 0; c < C; ++c)
+        if (lane * C + c >= LC - R) st_async_f64(dst + 8u * (lane * C + c - (LC - R)), v[c], bar);
+    }
   };
-  const int wl = warp > 0 ? warp - 1 : warp;       // strip edges read their own
-  const int wr = warp < NW - 1 ? warp + 1 : warp;  // buffers (invalid margin)
+  // edge-buffer columns of the left / right neighbour of this warp (the outer
+  // warps of a cluster tile read never-written zeros: invalid margin)
+  const int wl = warp;
+  const int wr = warp + 2;
+  // foreign edges of advance a (outer warps with a neighbour CTA): wait for
+  // the neighbour's st.async bytes of that advance
+  auto wait_foreign = [&](uint32_t a) {
+    if (CLU && (warp == 0 && cc.has_l()) || (warp == NW - 1 && cc.has_r()))
+      mbar_wait(&(warp == 0 ? fullL : fullR)[a & (NB - 1)], (a / NB) & 1);
+  };
+  // before an outer warp pushes advance a into the neighbour's slot, the
+  // neighbour must have released the slot's previous use (advance a - NB)
+  auto wait_slot_free = [&](uint32_t a) {
+    if (CLU && a >= (uint32_t)NB && ((warp == 0 && cc.has_l()) || (warp == NW - 1 && cc.has_r())))
+      mbar_wait(&(warp == 0 ? emptyL : emptyR)[a & (NB - 1)], ((a / NB) - 1) & 1);
+  };
+  // the last read of a foreign slot is LAG advances after it was produced:
+  // release it to the producer (relaxed: the values are in registers)
+  auto release_slot = [&](uint32_t a) {
+    if (CLU && lane == 0 && a >= (uint32_t)Cfg::LAG) {
+      const uint32_t j = (a - Cfg::LAG) & (NB - 1);
+      if (warp == 0 && cc.has_l())
+        mbar_arrive_remote_relaxed(mapa_shared(emptyR + j, cc.rank - 1));
+      if (warp == NW - 1 && cc.has_r())
+        mbar_arrive_remote_relaxed(mapa_shared(emptyL + j, cc.rank + 1));
+    }
+  };
+  // arm this advance's receive barriers (one arrival + the expected bytes)
+  auto arm_foreign = [&](uint32_t a) {
+    if (CLU && lane == 0 && ((warp == 0 && cc.has_l()) || (warp == NW - 1 && cc.has_r())))
+      mbar_arrive_expect_tx(&(warp == 0 ? fullL : fullR)[a & (NB - 1)], T * R * 8);
+  };
+  // advance done: local arrival; outer warps release the foreign slot whose
+  // last reader this advance was
+  auto arrive_adv = [&](uint32_t a) {
+    if (lane == 0) mbar_arrive(&advbar[a % Cfg::DR]);
+    release_slot(a);
+  };
 
   auto block = [&](int kbase, auto frows_tag) {
     constexpr bool FROWS = decltype(frows_tag)::value;
 #pragma unroll
     for (int uu = 0; uu < UW; ++uu) {
       const int k = kbase + uu;
-      const int bk = k & (NB - 1);
+      const int bk = adv & (NB - 1);  // edge-buffer slot of this advance
+      arm_foreign(adv);
+      wait_slot_free(adv);
       // (DR barriers round robin: advance a arrives on advbar[a % DR] as its
       // phase a / DR; waiting for advance adv-DR is then unambiguous)
       if (adv >= (uint32_t)Cfg::DR) {
@@ -198,7 +282,9 @@ __device__ __forceinline__ int halo2d_unit(const CUtensorMap* tm, double* __rest
           constexpr int dy = decltype(dI)::value - R;
           if constexpr (row_has_halo<SH>(dy)) {
             const int sl = SHIFT ? R + dy + uu : pmod<W>(uu - s * Z + dy);
-            const int xs = (k - Z + dy) & (NB - 1);  // advance that produced the row
+            const uint32_t ap = adv - (uint32_t)(Z - dy);  // advance that produced the row
+            const int xs = ap & (NB - 1);
+            if (CLU && adv >= (uint32_t)(Z - dy)) wait_foreign(ap);
             const double* Lb = xrow(s - 1, xs, wr, 0);   // right neighbour's left edge
             const double* Rb = xrow(s - 1, xs, wl, 1);   // left neighbour's right edge
             static_for<R>([&](auto jI) {
@@ -279,7 +365,7 @@ __device__ __forceinline__ int halo2d_unit(const CUtensorMap* tm, double* __rest
         }
       });
       __syncwarp();
-      if (lane == 0) mbar_arrive(&advbar[adv % Cfg::DR]);  // release covers the warp
+      arrive_adv(adv);  // (release covers the warp)
       ++adv;
     }
     if constexpr (SHIFT) {
@@ -329,7 +415,7 @@ __device__ __forceinline__ int halo2d_unit(const CUtensorMap* tm, double* __rest
       }
 #pragma unroll
       for (int c = 0; c < C; ++c) win[0][W - 1 + uu][c] = v[c];
-      push(0, k & (NB - 1), v);
+      push(0, (adv + uu) & (NB - 1), v);
     }
     static_for<T>([&](auto sI) {
       constexpr int s = decltype(sI)::value + 1;
@@ -352,7 +438,7 @@ __device__ __forceinline__ int halo2d_unit(const CUtensorMap* tm, double* __rest
         double b[2 * R + C];
 #pragma unroll
         for (int c = 0; c < C; ++c) b[R + c] = win[s - 1][R + uu][c];
-        const int xs = (k - Z) & (NB - 1);
+        const int xs = (adv + uu - Z) & (NB - 1);
         const double* Lb = xrow(s - 1, xs, wr, 0);
         const double* Rb = xrow(s - 1, xs, wl, 1);
         static_for<R>([&](auto jI) {
@@ -385,7 +471,7 @@ __device__ __forceinline__ int halo2d_unit(const CUtensorMap* tm, double* __rest
         if constexpr (s < T) {
 #pragma unroll
           for (int c = 0; c < C; ++c) win[s][W - 1 + uu][c] = nv[c];
-          push(s, k & (NB - 1), nv);
+          push(s, (adv + uu) & (NB - 1), nv);
         } else if (q >= r0 && q < r1 && !frow) {
           double* orow = out + (size_t)q * (size_t)pitch + (XW + lane * C);
 #pragma unroll
@@ -426,62 +512,97 @@ __device__ __forceinline__ int halo2d_unit(const CUtensorMap* tm, double* __rest
 }
 
 template <class SH, int T, int C, int NW, int S, bool EXACT, bool UNI, int MINB,
-          int SHIFT = 0>
+          int SHIFT = 0, bool CLU = false>
 __global__ void __launch_bounds__(NW * 32, MINB)
     k_halo2d(const __grid_constant__ TmapSet maps, const Halo2DArgs a,
              const __grid_constant__ Coefs<SH::NT> cf) {
   using Cfg = Halo2DCfg<SH, T, C, NW, S>;
+  constexpr int NB = Cfg::NB;
   extern __shared__ __align__(1024) unsigned char smem[];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   double* ring = reinterpret_cast<double*>(smem + warp * S * Cfg::ROW_BYTES);
   double* xh = reinterpret_cast<double*>(smem + Cfg::RING_BYTES);
-  uint64_t* bars_all = reinterpret_cast<uint64_t*>(smem + Cfg::RING_BYTES + Cfg::XH_DOUBLES * 8);
+  uint64_t* bars_all = reinterpret_cast<uint64_t*>(smem + Cfg::BAR_OFF);
   uint64_t* bars = bars_all + warp * S;
   uint64_t* advbar = bars_all + NW * S;
+  uint64_t* fullL = advbar + Cfg::DR;  // then fullR, emptyL, emptyR (NB each)
+  int* s_unit = reinterpret_cast<int*>(fullL + 4 * NB);
+
+  // cluster = device tile of CL CTA strips side by side (CL = 1: a lone CTA)
+  // (CLU = false: compiled for single-CTA tiles, no cluster code)
+  const int rank = CLU ? (int)cluster_ctarank() : 0;
+  const int CL = CLU ? (int)cluster_nctarank() : 1;
+  Halo2DCluster cc;
+  cc.rank = rank;
+  cc.n = CL;
 
   if (threadIdx.x == 0) {
     for (int i = 0; i < NW * S; ++i) mbar_init(&bars_all[i], 1);
     for (int i = 0; i < Cfg::DR; ++i) mbar_init(&advbar[i], NW);
+    // receive (our outer warp's expect_tx + the neighbour's bytes) and slot
+    // release (the neighbour's outer warp) barriers, NB each per side
+    for (int i = 0; i < 4 * NB; ++i) mbar_init(&fullL[i], 1);
     fence_mbarrier_init();
     prefetch_tmap(&maps.m[0]);
     prefetch_tmap(&maps.m[1]);
     prefetch_tmap(&maps.m[2]);
   }
-  // the edge buffers of the strip's outer warps are read but never written
+  // the edge buffers of the tile's outer warps are read but never written
   for (int i = threadIdx.x; i < Cfg::XH_DOUBLES; i += NW * 32) xh[i] = 0.0;
   __syncthreads();
+  // the neighbours' barriers must be initialised before anyone touches them
+  if (CL > 1) cluster_sync_all();
 
   const int n0 = a.n0, n1 = a.n1;
   const int units = a.nstrips * a.nseg;
+  const int LWc = CL * Cfg::LW;  // cluster tile width
   uint32_t ring_cnt = 0, adv = 0;
   int src = a.first_src, dst = a.first_dst;
-  __shared__ int s_unit;
   for (int e = 0; e < a.epochs; ++e) {
     const CUtensorMap* tm = &maps.m[src];
     double* __restrict__ out = (dst == BUF_OUT) ? a.buf[BUF_OUT] : a.buf[BUF_SCR];
     for (;;) {
-      if (threadIdx.x == 0) s_unit = atomicAdd(a.work + e, 1);
-      __syncthreads();
-      const int u = s_unit;
+      // rank 0 claims the next unit for the whole cluster tile
+      if (threadIdx.x == 0 && rank == 0) {
+        const int u = atomicAdd(a.work + e, 1);
+        *s_unit = u;
+        for (int r = 1; r < CL; ++r) st_cluster_u32(mapa_shared(s_unit, r), (uint32_t)u);
+      }
+      if (CL > 1)
+        cluster_sync_all();
+      else
+        __syncthreads();
+      const int u = *s_unit;
+      if (CL > 1)
+        cluster_sync_all();  // every rank has read it: the next claim may overwrite
+      else
+        __syncthreads();
       if (u >= units) break;
       const int strip = u % a.nstrips;
       const int seg = u / a.nstrips;
-      const StripGeom g =
-          stream2d_strip(strip, a.nstrips, a.aligned, n1, Cfg::LW, Cfg::VW, Cfg::HX, 2);
+      StripGeom g;
+      if (a.nstrips == 1 && LWc >= n1) {  // one tile spans the width: no margin
+        g.X0 = 0;
+        g.vlo = 0;
+        g.vhi = n1;
+      } else {
+        g = stream2d_strip(strip, a.nstrips, a.aligned, n1, LWc, LWc - 2 * Cfg::HX, Cfg::HX, 2);
+      }
+      const int X0 = g.X0 + rank * Cfg::LW;
+      const int vlo = max(g.vlo, X0), vhi = min(g.vhi, X0 + Cfg::LW);
       const int r0 = a.z_lo + seg * a.seg_len;
       const int r1 = min(a.z_hi, r0 + a.seg_len);
-      const bool edge = (g.X0 < Cfg::R) || (g.X0 + Cfg::LW > n1 - Cfg::R);
+      const bool edge = (X0 < Cfg::R) || (X0 + Cfg::LW > n1 - Cfg::R);
       int used;
       if (edge)
-        used = halo2d_unit<SH, T, C, NW, S, EXACT, UNI, true, SHIFT>(
-            tm, out, ring, bars, xh, advbar, ring_cnt, adv, warp, lane, n0, n1, a.pitch, g.X0, g.vlo,
-            g.vhi, r0, r1, cf);
+        used = halo2d_unit<SH, T, C, NW, S, EXACT, UNI, true, SHIFT, CLU>(
+            tm, out, ring, bars, xh, advbar, cc, ring_cnt, adv, warp, lane, n0, n1, a.pitch, X0,
+            vlo, vhi, r0, r1, cf);
       else
-        used = halo2d_unit<SH, T, C, NW, S, EXACT, UNI, false, SHIFT>(
-            tm, out, ring, bars, xh, advbar, ring_cnt, adv, warp, lane, n0, n1, a.pitch, g.X0, g.vlo,
-            g.vhi, r0, r1, cf);
+        used = halo2d_unit<SH, T, C, NW, S, EXACT, UNI, false, SHIFT, CLU>(
+            tm, out, ring, bars, xh, advbar, cc, ring_cnt, adv, warp, lane, n0, n1, a.pitch, X0,
+            vlo, vhi, r0, r1, cf);
       ring_cnt += (uint32_t)used;
-      __syncthreads();  // s_unit reuse; all warps done with the unit
     }
     if (e + 1 < a.epochs) {
       fence_proxy_async_global();
@@ -493,6 +614,8 @@ __global__ void __launch_bounds__(NW * 32, MINB)
     dst = (dst == BUF_OUT) ? BUF_SCR : BUF_OUT;
     src = nsrc;
   }
+  // no CTA may exit while a neighbour can still write its shared memory
+  if (CL > 1) cluster_sync_all();
 }
 
 }  // namespace ebisu

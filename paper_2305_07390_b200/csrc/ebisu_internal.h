@@ -41,6 +41,29 @@ cudaError_t launch_compare(const double* a, const double* b, long long n, long l
                            long long* first, double* max_abs, double* max_ref, cudaStream_t st,
                            int num_sms);
 
+// ---- resident-tile temporal blocking for any tap set (ebisu_generic.cu) ----
+// The grid is viewed as (planes, rows, cols) = ext[0..2]: 1-D (1, 1, n),
+// 2-D (1, n0, n1), 3-D (n0, n1, n2); grid axis 0 sits at tile axis zaxis.
+struct GenArgs {
+  long long ext[3];
+  long long pitch;       // row pitch (elements)
+  int zaxis;             // 3 - dims
+  long long z_lo, z_hi;  // output range along grid axis 0
+  int L[3], V[3], H[3];  // loaded / core / halo extents per tile axis
+  int RA[3];             // shrink per level (R on present axes, 0 on absent)
+  int F[3];              // frame width per axis
+  int nt[3];             // tiles per axis
+  int T;                 // fused levels of this launch
+  int ntaps;
+  int lin[EBISU_MAX_TAPS];  // tile-linear tap offsets
+  double coef[EBISU_MAX_TAPS];
+  const void* in;
+  void* out;
+};
+cudaError_t launch_generic_tb(const GenArgs& a, int elem, bool exact, int grid, int threads,
+                              int smem, cudaStream_t st);
+int generic_threads();
+
 // ---- temporal-blocking kernel registry -------------------------------------
 struct TbLaunch {
   // geometry
@@ -63,6 +86,7 @@ struct TbLaunch {
   long long* unit_clock;  // optional per-unit timing (profiling)
   int* work;              // per-epoch dynamic-scheduling counters (device)
   int* flags;             // per-unit completed-epoch flags (dataflow epochs) or null
+  int cluster = 1;        // halo2d: CTAs per cluster tile along axis 1 (device tile grid)
 };
 
 struct TbKernel {
@@ -86,6 +110,7 @@ struct TbKernel {
   int elem;              // element bytes: 8 (fp64) or 4 (fp32)
   int cluster = 1;       // CTAs per cluster along axis 1 (2: one tile over two SMs, DSMEM seam)
   cudaError_t (*max_clusters)(int*) = nullptr;  // resident clusters (cluster kernels)
+  cudaError_t (*max_clusters_n)(int, int*) = nullptr;  // halo2d: resident clusters of size n
 };
 
 // All instantiated temporal-blocking kernels (ebisu_registry.cu).

@@ -230,11 +230,12 @@ cudaError_t clusters_stream3d_cl(int* n) {
         &clusters_stream3d_cl<SH, T, CY, CX, NWY, S, (UNI) != 0, MINB>                        \
   }
 
-template <class SH, int T, int C, int NW, int S, bool EXACT, bool UNI, int MINB,
-          int SHIFT = 0>
+template <class SH, int T, int C, int NW, int S, bool EXACT, bool UNI, int MINB, int SHIFT,
+          bool CLU>
 cudaError_t launch_halo2d(const TbLaunch& L) {
   using Cfg = Halo2DCfg<SH, T, C, NW, S>;
-  auto kern = k_halo2d<SH, T, C, NW, S, EXACT, UNI, MINB, SHIFT>;
+  auto kern = k_halo2d<SH, T, C, NW, S, EXACT, UNI, MINB, SHIFT, CLU>;
+  if (!CLU && L.cluster != 1) return cudaErrorInvalidValue;
   cudaError_t err =
       cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg::SMEM_BYTES);
   if (err != cudaSuccess) return err;
@@ -257,13 +258,53 @@ cudaError_t launch_halo2d(const TbLaunch& L) {
   a.work = L.work;
   Coefs<SH::NT> cf;
   for (int i = 0; i < SH::NT; ++i) cf.c[i] = L.coeffs[i];
-  if (L.cooperative) {
-    void* args[] = {(void*)&maps, (void*)&a, (void*)&cf};
-    return cudaLaunchCooperativeKernel((const void*)kern, dim3(L.grid), dim3(NW * 32), args,
-                                       (size_t)Cfg::SMEM_BYTES, L.stream);
+  // clusters of L.cluster CTAs along x (the device tile), cooperative when
+  // the sweep has several epochs
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = dim3(L.grid);
+  cfg.blockDim = dim3(NW * 32);
+  cfg.dynamicSmemBytes = (size_t)Cfg::SMEM_BYTES;
+  cfg.stream = L.stream;
+  cudaLaunchAttribute attrs[2];
+  attrs[0].id = cudaLaunchAttributeClusterDimension;
+  attrs[0].val.clusterDim.x = (unsigned)L.cluster;
+  attrs[0].val.clusterDim.y = 1;
+  attrs[0].val.clusterDim.z = 1;
+  attrs[1].id = cudaLaunchAttributeCooperative;
+  attrs[1].val.cooperative = L.cooperative ? 1 : 0;
+  cfg.attrs = attrs;
+  cfg.numAttrs = 2;
+  if (L.cluster > 8) {
+    err = cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+    if (err != cudaSuccess) return err;
   }
-  kern<<<L.grid, NW * 32, Cfg::SMEM_BYTES, L.stream>>>(maps, a, cf);
-  return cudaGetLastError();
+  return cudaLaunchKernelEx(&cfg, kern, maps, a, cf);
+}
+
+// resident clusters of n CTAs (occupancy query for the planner)
+template <class SH, int T, int C, int NW, int S, bool EXACT, bool UNI, int MINB, int SHIFT>
+cudaError_t max_clusters_halo2d(int n, int* out) {
+  using Cfg = Halo2DCfg<SH, T, C, NW, S>;
+  auto kern = k_halo2d<SH, T, C, NW, S, EXACT, UNI, MINB, SHIFT, true>;
+  cudaError_t err =
+      cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg::SMEM_BYTES);
+  if (err != cudaSuccess) return err;
+  if (n > 8) {
+    err = cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+    if (err != cudaSuccess) return err;
+  }
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = dim3(n * 64);
+  cfg.blockDim = dim3(NW * 32);
+  cfg.dynamicSmemBytes = (size_t)Cfg::SMEM_BYTES;
+  cudaLaunchAttribute attr;
+  attr.id = cudaLaunchAttributeClusterDimension;
+  attr.val.clusterDim.x = (unsigned)n;
+  attr.val.clusterDim.y = 1;
+  attr.val.clusterDim.z = 1;
+  cfg.attrs = &attr;
+  cfg.numAttrs = 1;
+  return cudaOccupancyMaxActiveClusters(out, (const void*)kern, &cfg);
 }
 
 // box0 = warp columns (TMA box), valid_x = valid columns per CTA strip, C =
@@ -275,8 +316,20 @@ cudaError_t launch_halo2d(const TbLaunch& L) {
     SHAPE_ID, 2, T, C, NW, S, EX, UNI, Halo2DCfg<SH, T, C, NW, S>::SMEM_BYTES, 32 * C, 1, 1,   \
         Halo2DCfg<SH, T, C, NW, S>::VW, 0, Halo2DCfg<SH, T, C, NW, S>::Z,                     \
         Halo2DCfg<SH, T, C, NW, S>::LW,                                                       \
-        (const void*)&k_halo2d<SH, T, C, NW, S, (EX) != 0, (UNI) != 0, MINB, SHIFT>,          \
-        &launch_halo2d<SH, T, C, NW, S, (EX) != 0, (UNI) != 0, MINB, SHIFT>, 1, 8             \
+        (const void*)&k_halo2d<SH, T, C, NW, S, (EX) != 0, (UNI) != 0, MINB, SHIFT, false>,   \
+        &launch_halo2d<SH, T, C, NW, S, (EX) != 0, (UNI) != 0, MINB, SHIFT, false>, 1, 8      \
+  }
+// cluster-tile twin (device tile of several CTAs, DSMEM seam exchange):
+// registered after the single-CTA kernels; the planner picks it when the
+// device tile spans more than one CTA
+#define EBISU_H2D_ENTRY_CL(SHAPE_ID, SH, T, C, NW, S, EX, UNI, MINB, SHIFT)                    \
+  TbKernel {                                                                                  \
+    SHAPE_ID, 2, T, C, NW, S, EX, UNI, Halo2DCfg<SH, T, C, NW, S>::SMEM_BYTES, 32 * C, 1, 1,   \
+        Halo2DCfg<SH, T, C, NW, S>::VW, 0, Halo2DCfg<SH, T, C, NW, S>::Z,                     \
+        Halo2DCfg<SH, T, C, NW, S>::LW,                                                       \
+        (const void*)&k_halo2d<SH, T, C, NW, S, (EX) != 0, (UNI) != 0, MINB, SHIFT, true>,    \
+        &launch_halo2d<SH, T, C, NW, S, (EX) != 0, (UNI) != 0, MINB, SHIFT, true>, 1, 8, 1,   \
+        nullptr, &max_clusters_halo2d<SH, T, C, NW, S, (EX) != 0, (UNI) != 0, MINB, SHIFT>    \
   }
 
 }  // namespace ebisu

@@ -105,6 +105,11 @@ H2D_NW, H2D_S = 8, 8
 SHIFT_H2D = {"j2ds25pt": [(1, 4, 4), (2, 2, 4)]}  # (t, C, U): U=4 169 / 170, U=1 151 / 145
 # (halo j2d13pt with U=4 shifted windows: 311 / 323 vs rotating 326 / 351: rotating)
 SHIFT_H2D_AFTER = {}  # shifted variants registered after the rotating kernels
+# cluster-tile twins (device tiles of several CTAs exchanging seams through
+# DSMEM), bitwise shared-product kernels: (t, C, shift)
+H2D_CLU = {"j2d5pt": [(4, 4, 0), (8, 2, 0)], "j2d9pt_gol": [(2, 4, 0)], "j2d9pt": [(2, 4, 0)],
+           "j2d25pt": [(2, 4, 0)], "j2d13pt": [(2, 4, 0), (3, 4, 0)],
+           "j2ds25pt": [(1, 4, 4), (2, 2, 4)]}
 
 
 def h2d_minb(t, r, c, star):
@@ -249,6 +254,16 @@ def main():
                             for t, c, u in SHIFT_H2D_AFTER[tag]]
             _write_tu(arr, f"ebisu_inst_h2d_{tag}_{kind}.cu", tag, sh, entries)
             units.append(arr)
+    for sid, sh, tag, _ in H2D:
+        if tag not in H2D_CLU:
+            continue
+        star = sh.startswith("Star")
+        r = int(sh.split(",")[1].strip(" >)"))
+        arr = f"k_h2d_{tag}_c"
+        entries = [f"    EBISU_H2D_ENTRY_CL({sid}, SH_{tag}, {t}, {c}, {H2D_NW}, {H2D_S}, 1, 1, "
+                   f"{h2d_minb(t, r, c, star)}, {u}),\n" for t, c, u in H2D_CLU[tag]]
+        _write_tu(arr, f"ebisu_inst_h2d_{tag}_c.cu", tag, sh, entries)
+        units.append(arr)
     reg = [HEADER, '#include <vector>\n#include <mutex>\n#include "ebisu_internal.h"\n',
            "namespace ebisu {\n"]
     for arr in units:

@@ -106,17 +106,117 @@ def test_odd_width_runs_padded_tb_and_generic_shapes_use_naive_kernel():
     rev = eb.StencilShape("rev", 2, tuple(reversed(st.taps)), 2 * len(st.taps), 2,
                           len(st.taps) + 1, 4.0)
     g = eb.random_grid((40, 64), 9)
+    ref = oracle_run(g.cells, taps_of(rev), 7)
     out, tr = eb.sweep(g, rev, 7, trace=True)
-    assert tr["kernel"] == "naive_step"
-    assert np.array_equal(out.cells, oracle_run(g.cells, taps_of(rev), 7))
+    assert tr["kernel"] in ("resident_tb", "naive_step"), tr
+    assert np.array_equal(out.cells, ref)
+    for scheme, kern in ((_native.SCHEME_NAIVE, "naive_step"),
+                         (_native.SCHEME_RESIDENT, "resident_tb")):
+        out, tr = eb.sweep(g, rev, 7, scheme=scheme, trace=True)
+        assert tr["kernel"] == kern, tr
+        assert np.array_equal(out.cells, ref), kern
 
 
-def test_j1d3pt_naive_bitwise():
+def test_j1d3pt_bitwise_resident_and_naive():
     st = _shape("j1d3pt")
     g = eb.random_grid((301,), 77)
+    ref = oracle_run(g.cells, taps_of(st), 6)
     out, tr = eb.sweep(g, st, 6, trace=True)
+    assert tr["kernel"] in ("resident_tb", "naive_step"), tr  # planner's cost model
+    assert np.array_equal(out.cells, ref)
+    out, tr = eb.sweep(g, st, 6, scheme=_native.SCHEME_RESIDENT, trace=True)
+    assert tr["kernel"] == "resident_tb", tr
+    assert np.array_equal(out.cells, ref)
+    out, tr = eb.sweep(g, st, 6, scheme=_native.SCHEME_NAIVE, trace=True)
     assert tr["kernel"] == "naive_step"
-    assert np.array_equal(out.cells, oracle_run(g.cells, taps_of(st), 6))
+    assert np.array_equal(out.cells, ref)
+
+
+# ---- resident-tile kernel (any tap set, ebisu_generic.cu) ---------------------
+
+def _random_shape(rng, dims, rad):
+    """A user stencil the specialised kernels do not cover: random offsets
+    within radius `rad` (zero offset included, any order), random coefficients
+    (shapes.py:27-56 accepts any such tap set)."""
+    import itertools
+
+    box = [o for o in itertools.product(range(-rad, rad + 1), repeat=dims)]
+    n = 1 + rng.randint(1, min(len(box) - 1, 12))
+    picks = {tuple([0] * dims)}
+    edge = tuple([rad] + [0] * (dims - 1))  # the radius is attained
+    picks.add(edge)
+    while len(picks) < n:
+        picks.add(box[rng.randint(0, len(box) - 1)])
+    offs = list(picks)
+    # shuffle (tap order = summation order)
+    for i in range(len(offs) - 1, 0, -1):
+        j = rng.randint(0, i)
+        offs[i], offs[j] = offs[j], offs[i]
+    taps = tuple((o, 0.05 + 0.9 * rng.uniform() / len(offs)) for o in offs)
+    return eb.StencilShape("user", dims, taps, 2 * len(taps), 2, len(taps) + 1,
+                           float(min(4, len(taps) + 1)))
+
+
+@pytest.mark.parametrize("dims", [1, 2, 3])
+def test_resident_kernel_random_user_stencils_bitwise(dims):
+    """Random user tap sets (random offsets, order and coefficients) at every
+    depth 1..6 on ragged grids, odd extents included: bitwise equal to the
+    oracle (exact mode) and within 1e-12 in FMA mode."""
+    rng = eb.SplitMix64(0xC0FFEE + dims)
+    for case in range(6):
+        rad = 1 + rng.randint(0, 2)
+        st = _random_shape(rng, dims, rad)
+        if dims == 1:
+            ext = (2 * rad + 1 + rng.randint(0, 40000),)
+        elif dims == 2:
+            ext = (2 * rad + 1 + rng.randint(0, 300), 2 * rad + 1 + rng.randint(0, 300))
+        else:
+            ext = tuple(2 * rad + 1 + rng.randint(0, 40) for _ in range(3))
+        g = eb.random_grid(ext, rng.next_u64())
+        steps = rng.randint(1, 13)
+        ref = oracle_run(g.cells, taps_of(st), steps)
+        for t in (0, 1, 2, 3, 6):
+            out, tr = eb.sweep(g, st, steps, t=t, scheme=_native.SCHEME_RESIDENT, trace=True)
+            assert tr["kernel"] == "resident_tb", tr
+            assert np.array_equal(out.cells, ref), (dims, case, ext, steps, t, st.taps)
+        out = eb.sweep(g, st, steps, scheme=_native.SCHEME_RESIDENT, exact=False)
+        assert np.max(np.abs(out.cells - ref)) <= FMA_RTOL * np.max(np.abs(ref))
+        out = eb.sweep(g, st, steps, scheme=_native.SCHEME_RESIDENT, dtype=np.float32)
+        assert np.max(np.abs(out.cells - ref)) <= 1e-5 * np.max(np.abs(ref))
+
+
+@pytest.mark.parametrize("name", ["j1d3pt", "j2d5pt", "j2d9pt-gol", "j2d13pt", "j2ds25pt",
+                                  "j3d7pt", "j3d27pt", "poisson"])
+def test_resident_kernel_catalog_shapes_bitwise(name):
+    """The resident-tile kernel forced on catalog shapes (the specialised
+    kernels' cross-check), golden-size grids, depths 1..4."""
+    st = _shape(name)
+    r = st.radius
+    ext = {1: (50001,), 2: (257, 2 * r + 301), 3: (33, 2 * r + 29, 45)}[st.dims]
+    g = eb.random_grid(ext, 11)
+    ref = oracle_run(g.cells, taps_of(st), 9)
+    for t in (1, 2, 4):
+        out, tr = eb.sweep(g, st, 9, t=t, scheme=_native.SCHEME_RESIDENT, trace=True)
+        assert tr["kernel"] == "resident_tb" and tr["t_used"] == t, tr
+        assert np.array_equal(out.cells, ref), (name, t)
+
+
+def test_resident_kernel_output_plane_range():
+    """out_planes (the multi-GPU band / interior split) on the resident kernel:
+    only planes [lo, hi) are written, and they equal the full sweep's."""
+    from paper_2305_07390_b200 import device
+
+    torch = _torch()
+    rng = eb.SplitMix64(5)
+    st = _random_shape(rng, 2, 2)
+    d_in = device.random_grid_device((300, 200), seed=4)
+    full = device.sweep_device(d_in, st, 3, params=_native.make_params(
+        scheme=_native.SCHEME_RESIDENT, t=3))
+    out = torch.full_like(d_in, -7.0)
+    prm = _native.make_params(scheme=_native.SCHEME_RESIDENT, t=3, out_planes=(40, 170))
+    device.sweep_device(d_in, st, 3, out=out, params=prm)
+    assert torch.equal(out[40:170], full[40:170])
+    assert bool((out[:40] == -7.0).all()) and bool((out[170:] == -7.0).all())
 
 
 CASES_3D = {
@@ -584,3 +684,46 @@ def test_reassociated_full_size_against_bitwise_gpu(name, ext, steps):
     assert cmp["max_abs_diff"] <= FMA_RTOL * cmp["max_abs_ref"], cmp
     del a, b, s, d
     torch.cuda.empty_cache()
+
+
+# ---- device tiles of several CTAs (cluster halo exchange, k_halo2d CLU) ------
+
+@pytest.mark.parametrize("name,t", [("j2d5pt", 4), ("j2d5pt", 8), ("j2d9pt-gol", 2),
+                                    ("j2d9pt", 2), ("j2d25pt", 2), ("j2d13pt", 2),
+                                    ("j2d13pt", 3), ("j2ds25pt", 1), ("j2ds25pt", 2)])
+def test_device_tiles_of_cluster_ctas_bitwise(name, t):
+    """run_device_tiling with device_tile_grid = (1, CL): CL CTA strips per
+    device tile exchange their seam edges through DSMEM every level
+    (engine/device.py:145-211's per-step halo exchange); bitwise equal to the
+    oracle for widths below, at and above one tile, ragged strips included."""
+    st = _shape(name)
+    r = st.radius
+    rng = eb.SplitMix64(0xC1 + 7 * t + len(name))
+    for cl in (2, 4, 8):
+        for n1 in (2 * r + 2, 1024 * cl - 64, 1024 * cl, 2 * 1024 * cl + 4 * r + 38):
+            n0 = 2 * r + 1 + rng.randint(0, 200)
+            steps = t * rng.randint(1, 2)  # whole epochs: every stage is a halo stage
+            g = eb.random_grid((n0, n1), rng.next_u64())
+            ref = oracle_run(g.cells, taps_of(st), steps)
+            prm = _native.make_params(scheme=_native.SCHEME_DEVICE_TILING, t=t,
+                                      device_tile_grid=(1, cl))
+            out, tr = eb.sweep(g, st, steps, params=prm, trace=True)
+            assert tr["kernel"] == "halo2d_tb" and tr["cluster_ctas"] == cl, (cl, tr)
+            assert np.array_equal(out.cells, ref), (name, t, cl, (n0, n1), steps)
+
+
+def test_device_tiles_auto_cluster_full_width():
+    """AUTO device tiles on the config-3 geometry pick a cluster when it covers
+    the width with fewer computed columns; result bitwise equal to the
+    single-CTA tiles (which match the oracle, test_gpu_parity golden cases)."""
+    from paper_2305_07390_b200 import device
+
+    torch = _torch()
+    st = _shape("j2d13pt")
+    d_in = device.random_grid_device((1024, 8192), seed=2)
+    one = device.sweep_device(d_in, st, 6, params=_native.make_params(
+        scheme=_native.SCHEME_DEVICE_TILING, t=2, device_tile_grid=(1, 1)))
+    out, tr = device.sweep_device(d_in, st, 6, scheme=_native.SCHEME_DEVICE_TILING, t=2,
+                                  trace=True)
+    assert tr["kernel"] == "halo2d_tb"
+    assert torch.equal(out, one), tr
