@@ -316,6 +316,11 @@ def extra_configs(eb, device, _native, torch, stream, hbm_peak):
     st27 = eb.make_benchmark("j3d27pt")
     tr = _timed_sweep(device, torch, d3, st27, 500, o3, s3)
     rec("config4_j3d27pt_512", st27, ext3, 500, tr)
+    # tolerance mode (north star: 1e-12 relative; exact = 0): reassociated sums
+    for st_t in (st3, st27):
+        tr = _timed_sweep(device, torch, d3, st_t, 500, o3, s3, exact=False)
+        rec(f"config4_{st_t.name}_512_tol", st_t, ext3, 500, tr, arith=tr["arith"])
+        out[f"config4_{st_t.name}_512_tol"]["exact"] = False
     d3f = d3.float()
     del d3, o3, s3
     torch.cuda.empty_cache()
@@ -353,7 +358,24 @@ def extra_configs(eb, device, _native, torch, stream, hbm_peak):
                 tr = _timed_sweep(device, torch, d2, st, 96, o2, s2, t=t, scheme=scheme)
                 if best is None or tr["elapsed_ms"] < best["elapsed_ms"]:
                     best = tr
-            rec(f"config3_{name}_8192_{tag}", st, ext2, 96, best, scheme=tag)
+            rec(f"config3_{name}_8192_{tag}", st, ext2, 96, best, scheme=tag,
+                cluster_ctas=best.get("cluster_ctas", 1))
+        # device tiles of several CTAs (cluster halo exchange through DSMEM):
+        # the best cluster size of 2/4/8 at the best depth above
+        t_h = out[f"config3_{name}_8192_halo_exchange"]["fused_depth_t"]
+        best = None
+        for cl in (2, 4, 8):
+            prm = _native.make_params(scheme=_native.SCHEME_DEVICE_TILING, t=t_h,
+                                      device_tile_grid=(1, cl))
+            tr = _timed_sweep(device, torch, d2, st, 96, o2, s2, params=prm)
+            if best is None or tr["elapsed_ms"] < best["elapsed_ms"]:
+                best = tr
+        rec(f"config3_{name}_8192_halo_exchange_cluster", st, ext2, 96, best,
+            scheme="halo_exchange", cluster_ctas=best["cluster_ctas"])
+        # tolerance mode (reassociated sliding sums), planner's default scheme
+        tr = _timed_sweep(device, torch, d2, st, 96, o2, s2, exact=False)
+        rec(f"config3_{name}_8192_tol", st, ext2, 96, tr, arith=tr["arith"])
+        out[f"config3_{name}_8192_tol"]["exact"] = False
     # fp32 mode (north-star 1e-5 tolerance): configs 2 and 4 in binary32;
     # the naive roofline is then 8 B per cell-step
     st5 = eb.make_benchmark("j2d5pt")
@@ -369,6 +391,19 @@ def extra_configs(eb, device, _native, torch, stream, hbm_peak):
     tr = _timed_sweep(device, torch, d2, st5, 20, o2, s2, scheme=_native.SCHEME_NAIVE)
     rec("naive_j2d5pt_8192", st5, ext2, 20, tr)
     del d2, o2, s2
+    torch.cuda.empty_cache()
+    # 1-D (catalog j1d3pt, its default domain x4): the resident-tile kernel
+    # for tap sets without a specialised kernel vs one launch per step
+    st1 = eb.make_benchmark("j1d3pt")
+    ext1 = (4 * 8388608,)
+    d1 = device.random_grid_device(ext1, seed=1)
+    o1 = torch.empty_like(d1)
+    s1 = torch.empty_like(d1)
+    tr = _timed_sweep(device, torch, d1, st1, 256, o1, s1)
+    rec("j1d3pt_33554432_resident", st1, ext1, 256, tr)
+    tr = _timed_sweep(device, torch, d1, st1, 64, o1, s1, scheme=_native.SCHEME_NAIVE)
+    rec("j1d3pt_33554432_naive", st1, ext1, 64, tr)
+    del d1, o1, s1
     torch.cuda.empty_cache()
     return out
 
@@ -535,6 +570,19 @@ def main():
         line["e2e"] = {"value": cells_per_step * args.steps / dt / 1e9, "unit": "GCells/s",
                        "h2d_bytes_per_step": N0 * N1 * 8, "d2h_bytes_per_step": N0 * N1 * 8,
                        "api": "ebisu_run_host (pinned host buffers)"}
+        # the drop-in Python call a reference user makes: reference_run(Grid,
+        # stencil, t) on a pageable numpy grid (grid.py:106-113 signature)
+        g_host = eb.Grid(hin.copy(), "fixed-value")
+        eb.reference_run(g_host, st, args.tsteps)
+        t0 = time.perf_counter()
+        nref = 2
+        for _ in range(nref):
+            eb.reference_run(g_host, st, args.tsteps)
+        dt = time.perf_counter() - t0
+        line["e2e_reference_run"] = {
+            "value": cells_per_step * nref / dt / 1e9, "unit": "GCells/s",
+            "h2d_bytes_per_step": N0 * N1 * 8, "d2h_bytes_per_step": N0 * N1 * 8,
+            "api": "paper_2305_07390_b200.reference_run (pageable numpy Grid)", "calls": nref}
 
     if not args.no_sweep and world == 1:
         sweep = {}

@@ -79,7 +79,7 @@ def test_2d_shapes_all_depths_ragged(name):
             assert np.array_equal(out.cells, ref), (name, t, (n0, n1), steps, tr)
 
 
-def test_odd_width_runs_padded_tb_and_generic_shapes_use_naive_kernel():
+def test_odd_width_runs_padded_tb_and_generic_shapes_run_resident_or_naive():
     # odd row pitch (TMA needs 16-byte strides): the TB kernel runs on
     # row-padded copies; every depth, both schemes, fp64 + fp32 layouts
     st = _shape("j2d5pt")

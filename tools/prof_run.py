@@ -15,7 +15,9 @@ scheme = int(sys.argv[6]) if len(sys.argv) > 6 else 0
 # EBISU_EXACT=0: tolerance mode (reassociated kernels for uniform coefficients)
 prm = _native.make_params(scheme=scheme, t=t, variant=var,
                           persistent=os.environ.get("EBISU_PERSISTENT", "1") != "0",
-                          exact=os.environ.get("EBISU_EXACT", "1") != "0")
+                          exact=os.environ.get("EBISU_EXACT", "1") != "0",
+                          # EBISU_DTG=n: device tiles of n CTAs (cluster halo exchange)
+                          device_tile_grid=(1, int(os.environ.get("EBISU_DTG", "0"))))
 for _ in range(2):
     _, tr = device.sweep_device(d_in, st, steps, out=out, scratch=scr, params=prm, trace=True)
 print(tr)
