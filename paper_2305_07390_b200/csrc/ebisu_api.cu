@@ -13,8 +13,10 @@
 #include <stdlib.h>
 
 #include <algorithm>
+#include <array>
 #include <cmath>
 #include <mutex>
+#include <thread>
 #include <string>
 #include <vector>
 
@@ -1382,6 +1384,140 @@ static int32_t run_device_entry(const ebisu_stencil* stencil, int32_t ndim,
   return rc;
 }
 
+// ---- pageable host buffers: staged copies ---------------------------------------
+// The drop-in reference_run hands over pageable numpy arrays.  The driver's
+// pageable copies run single-threaded through its own bounce buffer, and a
+// fresh output array takes its page faults inside the D2H copy (measured:
+// 512 MiB H2D 48 ms, D2H 30 ms prefaulted / ~120 ms fresh, vs 10 + 10 ms
+// pinned).  Instead: a process-wide ring of pinned 16 MiB slots; host threads
+// copy chunks between the caller's array and the slots (faulting fresh pages
+// in parallel) while the DMA engine moves the previous group of slots.
+namespace staging {
+constexpr size_t kChunk = 16u << 20;
+struct Pool {
+  std::mutex mu;  // one staged transfer at a time (concurrent calls queue here)
+  std::vector<void*> slots;
+  std::vector<cudaEvent_t> done;
+  int dev = -1;
+};
+Pool& pool() {
+  static Pool p;
+  return p;
+}
+int threads() {
+  const unsigned hw = std::thread::hardware_concurrency();
+  return (int)std::max(2u, std::min(8u, hw ? hw / 2 : 2u));
+}
+bool pageable(const void* p) {
+  cudaPointerAttributes a;
+  if (cudaPointerGetAttributes(&a, p) != cudaSuccess) {
+    cudaGetLastError();
+    return true;
+  }
+  return a.type == cudaMemoryTypeUnregistered;
+}
+// (caller holds the pool lock) ensure 2*K pinned slots on the current device
+cudaError_t ensure(Pool& P, int K) {
+  int dev = 0;
+  cudaError_t e = cudaGetDevice(&dev);
+  if (e != cudaSuccess) return e;
+  if (P.dev != dev) {
+    for (void* q : P.slots) cudaFreeHost(q);
+    for (cudaEvent_t ev : P.done) cudaEventDestroy(ev);
+    P.slots.clear();
+    P.done.clear();
+    P.dev = dev;
+  }
+  while ((int)P.slots.size() < 2 * K) {
+    void* q = nullptr;
+    cudaEvent_t ev;
+    if ((e = cudaMallocHost(&q, kChunk)) != cudaSuccess) return e;
+    if ((e = cudaEventCreateWithFlags(&ev, cudaEventDisableTiming)) != cudaSuccess) {
+      cudaFreeHost(q);
+      return e;
+    }
+    P.slots.push_back(q);
+    P.done.push_back(ev);
+  }
+  return cudaSuccess;
+}
+// parallel memcpy of up to K (dst, src, len) jobs
+void par_copy(const std::vector<std::array<size_t, 3>>& jobs) {
+  std::vector<std::thread> th;
+  for (size_t i = 1; i < jobs.size(); ++i)
+    th.emplace_back([&jobs, i] {
+      memcpy((void*)jobs[i][0], (const void*)jobs[i][1], jobs[i][2]);
+    });
+  if (!jobs.empty()) memcpy((void*)jobs[0][0], (const void*)jobs[0][1], jobs[0][2]);
+  for (auto& t : th) t.join();
+}
+cudaError_t h2d(void* d, const void* h, size_t bytes, cudaStream_t st) {
+  Pool& P = pool();
+  std::lock_guard<std::mutex> lk(P.mu);
+  const int K = threads();
+  cudaError_t e = ensure(P, K);
+  if (e != cudaSuccess) return e;
+  const size_t nch = (bytes + kChunk - 1) / kChunk;
+  for (size_t g = 0; g < nch; g += K) {
+    std::vector<std::array<size_t, 3>> jobs;
+    for (size_t c = g; c < std::min(nch, g + K); ++c) {
+      const int slot = (int)(c % (2 * K));
+      // the slot's previous DMA (2K chunks ago) must have drained
+      if ((e = cudaEventSynchronize(P.done[slot])) != cudaSuccess) return e;
+      const size_t off = c * kChunk, len = std::min(kChunk, bytes - off);
+      jobs.push_back({(size_t)P.slots[slot], (size_t)h + off, len});
+    }
+    par_copy(jobs);
+    for (size_t c = g; c < std::min(nch, g + K); ++c) {
+      const int slot = (int)(c % (2 * K));
+      const size_t off = c * kChunk, len = std::min(kChunk, bytes - off);
+      if ((e = cudaMemcpyAsync((char*)d + off, P.slots[slot], len, cudaMemcpyHostToDevice, st)) !=
+          cudaSuccess)
+        return e;
+      if ((e = cudaEventRecord(P.done[slot], st)) != cudaSuccess) return e;
+    }
+  }
+  // the slots stay referenced by queued DMA: drain before releasing the pool
+  for (cudaEvent_t ev : P.done)
+    if ((e = cudaEventSynchronize(ev)) != cudaSuccess) return e;
+  return cudaSuccess;
+}
+cudaError_t d2h(void* h, const void* d, size_t bytes, cudaStream_t st) {
+  Pool& P = pool();
+  std::lock_guard<std::mutex> lk(P.mu);
+  const int K = threads();
+  cudaError_t e = ensure(P, K);
+  if (e != cudaSuccess) return e;
+  const size_t nch = (bytes + kChunk - 1) / kChunk;
+  auto issue = [&](size_t g) -> cudaError_t {
+    for (size_t c = g; c < std::min(nch, g + K); ++c) {
+      const int slot = (int)(c % (2 * K));
+      const size_t off = c * kChunk, len = std::min(kChunk, bytes - off);
+      cudaError_t r = cudaMemcpyAsync(P.slots[slot], (const char*)d + off, len,
+                                      cudaMemcpyDeviceToHost, st);
+      if (r == cudaSuccess) r = cudaEventRecord(P.done[slot], st);
+      if (r != cudaSuccess) return r;
+    }
+    return cudaSuccess;
+  };
+  if (nch > 0 && (e = issue(0)) != cudaSuccess) return e;
+  for (size_t g = 0; g < nch; g += K) {
+    // DMA of the next group into the other half of the ring overlaps the
+    // host copies of this one
+    if (g + K < nch && (e = issue(g + K)) != cudaSuccess) return e;
+    std::vector<std::array<size_t, 3>> jobs;
+    for (size_t c = g; c < std::min(nch, g + K); ++c) {
+      const int slot = (int)(c % (2 * K));
+      if ((e = cudaEventSynchronize(P.done[slot])) != cudaSuccess) return e;
+      const size_t off = c * kChunk, len = std::min(kChunk, bytes - off);
+      jobs.push_back({(size_t)h + off, (size_t)P.slots[slot], len});
+    }
+    par_copy(jobs);
+  }
+  return cudaSuccess;
+}
+}  // namespace staging
+
 static int32_t run_host_entry(const ebisu_stencil* stencil, int32_t ndim,
                               const int64_t* extents, const void* in, void* out, int64_t steps,
                               const ebisu_params* params, ebisu_trace* trace, int elem) {
@@ -1403,11 +1539,16 @@ static int32_t run_host_entry(const ebisu_stencil* stencil, int32_t ndim,
     cudaFreeAsync(d_in, st);
     return cuda_fail(e, "cudaMallocAsync(out)");
   }
-  e = cudaMemcpyAsync(d_in, in, bytes, cudaMemcpyHostToDevice, st);
+  // pageable (e.g. numpy) buffers: staged through pinned slots by host threads
+  const bool stage_in = staging::pageable(in), stage_out = staging::pageable(out);
+  e = stage_in ? staging::h2d(d_in, in, bytes, st)
+               : cudaMemcpyAsync(d_in, in, bytes, cudaMemcpyHostToDevice, st);
   if (e == cudaSuccess) {
     rc = run_device_entry(stencil, ndim, extents, d_in, d_out, nullptr, steps, params, st, trace,
                           elem);
-    if (!rc) e = cudaMemcpyAsync(out, d_out, bytes, cudaMemcpyDeviceToHost, st);
+    if (!rc)
+      e = stage_out ? staging::d2h(out, d_out, bytes, st)
+                    : cudaMemcpyAsync(out, d_out, bytes, cudaMemcpyDeviceToHost, st);
   }
   if (e == cudaSuccess) e = cudaStreamSynchronize(st);
   cudaFreeAsync(d_in, st);
