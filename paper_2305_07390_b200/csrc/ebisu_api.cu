@@ -318,7 +318,6 @@ bool uniform_coeffs(const ProblemDesc& p) {
 int default_depth_tol(int shape_id, int exact_default) {
   switch (shape_id) {
     case SHAPE_J2D13PT: return 2;
-    case SHAPE_J2D9PT: return 3;
     default: return exact_default;
   }
 }
@@ -328,7 +327,7 @@ int default_depth(int shape_id) {
     case SHAPE_J2D5PT: return 8;
     case SHAPE_J2D9PT_GOL: return 6;
     case SHAPE_J2D9PT: return 4;
-    case SHAPE_J2D25PT: return 3;
+    case SHAPE_J2D25PT: return 2;  // t=1/2/3/4: 293/330/248/202 (tools/tune_depths.py)
     case SHAPE_J2D13PT: return 3;
     case SHAPE_J2DS25PT: return 1;
     case SHAPE_J3D7PT: return 4;
@@ -984,15 +983,9 @@ bool gen_plan(const ProblemDesc& p, int T, int sms, GenPlan* out) {
 // no register reuse between taps).  Forced (scheme RESIDENT) without a depth:
 // the measured-best depth per dimensionality.
 int gen_pick_depth(const ProblemDesc& p, int t_req, int sms, bool forced) {
+  if (!forced && p.dims >= 2) return 0;  // 2-D/3-D: one launch per step is faster
   int want = t_req;
-  if (want <= 0) {
-    if (p.dims == 1)
-      want = 16;
-    else if (forced)
-      want = p.dims == 2 ? 8 : 2;
-    else
-      return 0;
-  }
+  if (want <= 0) want = p.dims == 1 ? 16 : (p.dims == 2 ? 8 : 2);
   for (int T = want; T >= 1; --T) {
     GenPlan g;
     if (gen_plan(p, T, sms, &g)) return T;
@@ -1090,6 +1083,15 @@ int run_device_impl(const ProblemDesc& p0, const void* d_in, void* d_out, void* 
     if (!k && (want_c || want_v))
       return fail(EBISU_ERR_UNSUPPORTED, "no kernel with depth %d, %d cells per lane, variant %d",
                   t, want_c, want_v);
+    if (!k && fam == 1) {
+      // no halo-exchange kernel of this depth: the overlapped kernel of the
+      // same depth computes the identical result
+      const TbKernel* k0 = find_tb(p.shape_id, D, t, exact, uni, 0, p.elem);
+      if (k0 && best_depth_leq(p.shape_id, D, t, exact, uni, 1, p.elem) == 0) {
+        fam = 0;
+        k = k0;
+      }
+    }
     if (!k) {
       // depth not instantiated: compose the sweep from the deepest kernel
       // below it (epochs compose bitwise, test_grid.py:94-117)

@@ -1,3 +1,3 @@
 set -x; mkdir -p gpurun_out
-timeout 600 python tools/e2e_breakdown.py > gpurun_out/e2e.log 2>&1
-timeout 900 python -m pytest tests/test_gpu_parity.py -x -q -k "golden or concurrent or purity or odd_width or fp32_within" > gpurun_out/host_tests.log 2>&1; echo "rc=$?" >> gpurun_out/host_tests.log
+timeout 300 python -c "import __graft_entry__ as g; g.smoke()" > gpurun_out/smoke.log 2>&1; echo "rc=$?" >> gpurun_out/smoke.log
+timeout 1500 python -m pytest tests -m gpu -x -q > gpurun_out/r02_gputest3.log 2>&1; echo "rc=$?" >> gpurun_out/r02_gputest3.log
