@@ -58,7 +58,8 @@
 extern "C" {
 #endif
 
-#define EBISU_ABI_VERSION 2  /* 2: ebisu_params.frame_ready, fp32 entry points */
+#define EBISU_ABI_VERSION 3  /* 2: ebisu_params.frame_ready, fp32 entry points;
+                                 3: ebisu_params.reserve_sms, trace.cluster_ctas */
 #define EBISU_MAX_DIMS 3
 #define EBISU_MAX_TAPS 128
 
@@ -116,6 +117,11 @@ typedef struct ebisu_params {
   int32_t frame_ready;       /* 1: d_out (and d_scratch) already hold the input's
                                 Dirichlet frame, skip the frame pre-copy (repeated
                                 epochs into the same buffers) */
+  int32_t reserve_sms;       /* leave this many SMs free of the sweep's persistent
+                                grid (0 = none): kernels issued concurrently on
+                                other streams -- the multi-GPU driver's NCCL halo
+                                exchange -- then run beside the interior instead
+                                of queueing behind it */
 } ebisu_params;
 /* Shared products: when every coefficient of the stencil is bitwise equal (the
  * catalog default 1/|taps|, shapes.py:148-157), term_k = RN(c*x_k) depends on

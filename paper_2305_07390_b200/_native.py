@@ -31,7 +31,7 @@ SCHEME_DEVICE_TILING = 3
 SCHEME_RESIDENT = 4  # resident tiles, runtime taps (any stencil)
 
 # Every symbol include/ebisu.h declares (checked by tests/test_native_abi.py).
-ABI_VERSION = 2  # include/ebisu.h EBISU_ABI_VERSION (ParamsC layout below)
+ABI_VERSION = 3  # include/ebisu.h EBISU_ABI_VERSION (ParamsC layout below)
 
 EXPORTS = (
     "ebisu_abi_version",
@@ -82,6 +82,7 @@ class ParamsC(ctypes.Structure):
         ("per_tap_products", ctypes.c_int32),
         ("out_planes", ctypes.c_int32 * 2),
         ("frame_ready", ctypes.c_int32),
+        ("reserve_sms", ctypes.c_int32),
     ]
 
 
@@ -210,7 +211,7 @@ def make_params(scheme: int = SCHEME_AUTO, t: int = 0, tile=(0, 0), device_tile_
                 validate_tile: bool = False, lane_cells: int = 0,
                 seg_rows: int = 0, variant: int = 0,
                 per_tap_products: bool = False, out_planes=(0, 0),
-                frame_ready: bool = False) -> ParamsC:
+                frame_ready: bool = False, reserve_sms: int = 0) -> ParamsC:
     p = ParamsC()
     p.scheme = scheme
     p.t = int(t)
@@ -228,6 +229,7 @@ def make_params(scheme: int = SCHEME_AUTO, t: int = 0, tile=(0, 0), device_tile_
     p.per_tap_products = int(bool(per_tap_products))
     p.out_planes[0], p.out_planes[1] = int(out_planes[0]), int(out_planes[1])
     p.frame_ready = int(bool(frame_ready))
+    p.reserve_sms = int(reserve_sms)
     return p
 
 

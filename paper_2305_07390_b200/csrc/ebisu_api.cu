@@ -124,6 +124,7 @@ int validate(const ebisu_stencil* st, int ndim, const int64_t* ext, const ebisu_
     if (prm->scheme < EBISU_SCHEME_AUTO || prm->scheme > EBISU_SCHEME_RESIDENT)
       return fail(EBISU_ERR_PARAM, "unknown scheme %d", prm->scheme);
     if (prm->t < 0) return fail(EBISU_ERR_PARAM, "temporal depth must be >= 1");
+    if (prm->reserve_sms < 0) return fail(EBISU_ERR_PARAM, "reserve_sms must be >= 0");
     if (prm->out_planes[1] != 0 &&
         (prm->out_planes[0] < 0 || prm->out_planes[0] >= prm->out_planes[1] ||
          prm->out_planes[1] > ext[0]))
@@ -614,7 +615,7 @@ int run_halo2d_stage(const ProblemDesc& p, const TbKernel* k, int epochs, int fi
       if (c > 1) {
         int ncl = 0;
         EB_CUDA(kc->max_clusters_n(c, &ncl));
-        slots = ncl * c;
+        slots = std::min(ncl * c, per_sm * di.sms / c * c);  // (reserve_sms)
       }
       if (slots < c) continue;
       int al = 0;
@@ -730,7 +731,7 @@ int run_tb3d_stage(const ProblemDesc& p, const TbKernel* k, int epochs, int firs
     int nclusters = 0;
     EB_CUDA(k->max_clusters(&nclusters));
     if (nclusters < 1) return fail(EBISU_ERR_CUDA, "cluster kernel cannot be resident (T=%d)", T);
-    max_ctas = nclusters * cl;
+    max_ctas = std::min(nclusters * cl, std::max(cl, max_ctas / cl * cl));  // (reserve_sms)
   }
   // edge-aligned tiles when two fit along an axis (stream2d_strip geometry)
   auto tiles_along = [](int n, int L, int V, int* aligned, int AL) {
@@ -1040,6 +1041,9 @@ int run_device_impl(const ProblemDesc& p0, const void* d_in, void* d_out, void* 
   DevInfo di;
   int rc = device_info(&di);
   if (rc) return rc;
+  // SMs left free for concurrent kernels on other streams (at least one SM
+  // stays with the sweep)
+  if (prm && prm->reserve_sms > 0) di.sms = std::max(1, di.sms - prm->reserve_sms);
   const long long total = p.ext[0] * p.ext[1] * p.ext[2];
   const size_t bytes = (size_t)total * (size_t)p.elem;
   if (steps == 0) {

@@ -75,17 +75,23 @@ def slab_plan(n0: int, world: int, rank: int, halo: int) -> SlabPlan:
     return SlabPlan(rank, world, n0, own0, own1, lo, hi)
 
 
+# SMs the interior kernel leaves to NCCL's point-to-point kernels (one or two
+# CTAs per channel and peer) -- see SlabSweep.__init__
+INTERIOR_RESERVE_SMS = 2
+
+
 def _default_step(stencil: StencilShape, exact: bool):
     from . import _native, device
 
-    def step(src, dst, scratch, steps, t, planes=None, frame_ready=False):
+    def step(src, dst, scratch, steps, t, planes=None, frame_ready=False, reserve_sms=0):
         if planes is None:
             device.sweep_device(src, stencil, steps, out=dst, scratch=scratch, t=t, exact=exact)
         else:
             # frame_ready: dst already holds the (constant) frame, so the
-            # ranged call skips its frame pre-copy launch
+            # ranged call skips its frame pre-copy launch; reserve_sms keeps
+            # SMs free of the interior grid for the concurrent NCCL kernels
             prm = _native.make_params(t=t, exact=exact, out_planes=planes,
-                                      frame_ready=frame_ready)
+                                      frame_ready=frame_ready, reserve_sms=reserve_sms)
             device.sweep_device(src, stencil, steps, out=dst, params=prm)
 
     return step
@@ -118,6 +124,13 @@ class SlabSweep:
             torch.device("cuda", torch.cuda.current_device()) if torch.cuda.is_available()
             else torch.device("cpu"))
         self.step = step if step is not None else _default_step(stencil, exact)
+        # The interior grid is persistent (one CTA per SM): if it held every
+        # SM, the NCCL send/recv kernels of the band exchange (launched on the
+        # communication stream behind the band kernels) could not start until
+        # the interior finished, and the exchange would serialise behind it.
+        # INTERIOR_RESERVE_SMS SMs stay free for them (1.4 % of the interior's
+        # throughput at 2 of 148).
+        self._interior_kw = {"reserve_sms": INTERIOR_RESERVE_SMS} if step is None else {}
         rest = self.extents[1:]
         shape = (self.plan.local_planes,) + rest
         plane = 1
@@ -253,7 +266,8 @@ class SlabSweep:
 
         def interior():
             if inner[1] > inner[0]:
-                self.step(self.a, self.b, None, t, t, planes=inner, frame_ready=ready)
+                self.step(self.a, self.b, None, t, t, planes=inner, frame_ready=ready,
+                          **self._interior_kw)
                 self.kernel_launches += per_call
 
         if self.comm is not None:

@@ -727,3 +727,50 @@ def test_device_tiles_auto_cluster_full_width():
                                   trace=True)
     assert tr["kernel"] == "halo2d_tb"
     assert torch.equal(out, one), tr
+
+
+def test_host_entry_pageable_and_pinned_buffers_agree():
+    """ebisu_run_host stages pageable (numpy) buffers through its pinned slot
+    ring with host threads: multi-chunk sizes that are not a multiple of the
+    16 MiB slot, fresh (unfaulted) outputs, aliasing in == out on the host,
+    and pinned buffers (direct DMA) all give the same bitwise result."""
+    import ctypes
+
+    torch = _torch()
+    st = _shape("j2d5pt")
+    lib = _native.load()
+    sa = _native.StencilArgs(st)
+    for ext in ((3001, 1003), (64, 2 * (1 << 21) + 2)):  # 24 MiB, 2 x 16 MiB + 16 B
+        g = eb.random_grid(ext, 21)
+        ref = eb.sweep(g, st, 9, t=4).cells  # pageable in, fresh pageable out
+        src = np.ascontiguousarray(g.cells)
+        pin_in = torch.from_numpy(src).pin_memory()
+        pin_out = torch.empty_like(pin_in).pin_memory()
+        prm = _native.make_params(t=4)
+        rc = lib.ebisu_run_host(ctypes.byref(sa.c), 2, _native.extents_c(ext),
+                                pin_in.data_ptr(), pin_out.data_ptr(), 9, ctypes.byref(prm), None)
+        assert rc == 0, _native.last_error()
+        assert np.array_equal(pin_out.numpy(), ref), ext
+        inplace = src.copy()  # in == out on the host (allowed by the ABI)
+        rc = lib.ebisu_run_host(ctypes.byref(sa.c), 2, _native.extents_c(ext),
+                                inplace.ctypes.data, inplace.ctypes.data, 9, ctypes.byref(prm), None)
+        assert rc == 0, _native.last_error()
+        assert np.array_equal(inplace, ref), ext
+        if ext[0] > 100:  # (the oracle on the 2^28-cell case would take minutes)
+            assert np.array_equal(ref, oracle_run(g.cells, taps_of(st), 9))
+
+
+def test_reserve_sms_shrinks_the_persistent_grid():
+    """ebisu_params.reserve_sms (the multi-GPU interior call keeps SMs free
+    for the concurrent NCCL kernels): fewer resident CTAs, same bits."""
+    from paper_2305_07390_b200 import device
+
+    torch = _torch()
+    for name, ext in (("j2d5pt", (2048, 2048)), ("j3d7pt", (128, 512, 512))):
+        st = _shape(name)
+        d_in = device.random_grid_device(ext, seed=8)
+        full, tr0 = device.sweep_device(d_in, st, 8, params=_native.make_params(t=4), trace=True)
+        part, tr1 = device.sweep_device(d_in, st, 8, params=_native.make_params(
+            t=4, reserve_sms=20), trace=True)
+        assert torch.equal(full, part), name
+        assert tr1["grid_ctas"] < tr0["grid_ctas"], (name, tr0["grid_ctas"], tr1["grid_ctas"])

@@ -45,7 +45,7 @@ def test_abi_version_and_kernel_names():
     if not os.path.exists(_native.LIB_PATH):
         pytest.skip("libebisu.so not built")
     lib = _native.load()
-    assert lib.ebisu_abi_version() == 2
+    assert lib.ebisu_abi_version() == 3
     assert _native.kernel_name(2) == "stream2d_tb"
     assert _native.kernel_name(1) == "naive_step"
 

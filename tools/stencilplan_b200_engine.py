@@ -39,7 +39,8 @@ class _Params(ctypes.Structure):  # ebisu_params
                 ("persistent", ctypes.c_int32), ("validate_tile", ctypes.c_int32),
                 ("lane_cells", ctypes.c_int32), ("seg_rows", ctypes.c_int32),
                 ("variant", ctypes.c_int32), ("per_tap_products", ctypes.c_int32),
-                ("out_planes", ctypes.c_int32 * 2), ("frame_ready", ctypes.c_int32)]
+                ("out_planes", ctypes.c_int32 * 2), ("frame_ready", ctypes.c_int32),
+                ("reserve_sms", ctypes.c_int32)]
 
 
 class _Trace(ctypes.Structure):  # ebisu_trace
@@ -48,7 +49,8 @@ class _Trace(ctypes.Structure):  # ebisu_trace
         "syncs_device", "cells_computed", "cells_valid", "device_tiles",
         "kernel_launches")] + [("elapsed_ms", ctypes.c_double)] + [
         (n, ctypes.c_int32) for n in ("kernel_id", "t_used", "grid_ctas",
-                                      "warps_per_cta", "arith")] + [("reserved", ctypes.c_int32 * 3)]
+                                      "warps_per_cta", "arith", "cluster_ctas")] + [
+        ("reserved", ctypes.c_int32 * 2)]
 
 
 _lib = ctypes.CDLL(_LIB)
