@@ -1,2 +1,2 @@
 set -x; mkdir -p gpurun_out
-timeout 900 python -m pytest tests -m gpu -x -q -k "reserve or host_entry or distributed or slab" > gpurun_out/r02_gputest5.log 2>&1; echo "rc=$?" >> gpurun_out/r02_gputest5.log
+EBISU_LIB_PATH=$PWD/scratch/libebisu_exp.so timeout 300 python tools/clu_bench.py > gpurun_out/clu_exp.log 2>&1
