@@ -865,6 +865,7 @@ struct GenPlan {
 
 bool gen_plan(const ProblemDesc& p, int T, int sms, GenPlan* out) {
   const int D = p.dims, R = p.rad;
+  if (T < 1 || T > EBISU_GEN_MAXT) return false;
   GenArgs a;
   memset(&a, 0, sizeof(a));
   for (int ax = 0; ax < 3; ++ax) a.ext[ax] = 1;
@@ -958,6 +959,11 @@ bool gen_plan(const ProblemDesc& p, int T, int sms, GenPlan* out) {
   if (best >= 1e300) return false;
   a = bestA;
   a.ntaps = p.ntaps;
+  for (int lv = 1; lv <= T; ++lv) {  // the kernel's per-level row/chunk divisors
+    const int w1 = a.L[1] - 2 * lv * a.RA[1], w2 = a.L[2] - 2 * lv * a.RA[2];
+    a.lvl_cpr[lv - 1] = gen_div((uint32_t)std::max(1, (w2 + 127) / 128));
+    a.lvl_w1[lv - 1] = gen_div((uint32_t)std::max(1, w1));
+  }
   for (int k = 0; k < p.ntaps; ++k) {
     const int* o = p.offsets + k * D;
     int off[3] = {0, 0, 0};
@@ -985,7 +991,7 @@ bool gen_plan(const ProblemDesc& p, int T, int sms, GenPlan* out) {
 // the measured-best depth per dimensionality.
 int gen_pick_depth(const ProblemDesc& p, int t_req, int sms, bool forced) {
   if (!forced && p.dims >= 2) return 0;  // 2-D/3-D: one launch per step is faster
-  int want = t_req;
+  int want = std::min(t_req, EBISU_GEN_MAXT);
   if (want <= 0) want = p.dims == 1 ? 16 : (p.dims == 2 ? 8 : 2);
   for (int T = want; T >= 1; --T) {
     GenPlan g;

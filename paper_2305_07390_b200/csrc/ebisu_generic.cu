@@ -39,7 +39,7 @@
 
 namespace ebisu {
 
-constexpr int kGenThreads = 512;
+constexpr int kGenThreads = 1024;
 
 // cp.async of one element, zero-filled when !pred (src-size 0)
 template <class E>
@@ -52,15 +52,17 @@ constexpr int kGenCPL = 4;  // cells per lane per row chunk
 constexpr int kGenPad = 32 * kGenCPL;  // elements after each buffer (idle lanes read there)
 
 // n / d for 0 <= n < 2^31 by a block-uniform d >= 1 (Granlund-Montgomery:
-// one mul.hi, an add and two shifts instead of the ~20-instruction division)
+// one mul.hi, an add and two shifts instead of the ~20-instruction division);
+// the per-level divisors come precomputed from the host (GenArgs.lvl_*), the
+// per-tile ones are derived once per tile
 struct FastDiv {
-  uint32_t d, m, s1, s2;
-  __device__ __forceinline__ explicit FastDiv(uint32_t dv) : d(dv) {
-    uint32_t l = 0;
-    while ((1u << l) < dv) ++l;  // l = ceil(log2 d)
-    m = (uint32_t)((((uint64_t)1 << 32) * (((uint64_t)1 << l) - dv)) / dv) + 1;
-    s1 = l > 0 ? 1 : 0;
-    s2 = l > 0 ? l - 1 : 0;
+  uint32_t m, s1, s2;
+  __device__ __forceinline__ explicit FastDiv(const GenDiv& g) : m(g.m), s1(g.s1), s2(g.s2) {}
+  __device__ __forceinline__ explicit FastDiv(uint32_t dv) {
+    const GenDiv g = gen_div(dv);
+    m = g.m;
+    s1 = g.s1;
+    s2 = g.s2;
   }
   __device__ __forceinline__ uint32_t div(uint32_t n) const {
     const uint32_t t = __umulhi(n, m);
@@ -150,7 +152,7 @@ __global__ void __launch_bounds__(kGenThreads, 1) k_generic_tb(const __grid_cons
       const int w1 = hi1 - lo1, w2 = hi2 - lo2;
       const int cpr = (w2 + CH - 1) / CH;
       const int nch = (hi0 - lo0) * w1 * cpr;
-      const FastDiv dcpr((uint32_t)cpr), dw1((uint32_t)w1);
+      const FastDiv dcpr(a.lvl_cpr[s - 1]), dw1(a.lvl_w1[s - 1]);
       for (int c = warp; c < nch; c += NW) {
         const int row = (int)dcpr.div((uint32_t)c);
         const int xb = lo2 + (c - row * cpr) * CH + lane;

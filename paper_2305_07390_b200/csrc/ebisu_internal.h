@@ -44,6 +44,21 @@ cudaError_t launch_compare(const double* a, const double* b, long long n, long l
 // ---- resident-tile temporal blocking for any tap set (ebisu_generic.cu) ----
 // The grid is viewed as (planes, rows, cols) = ext[0..2]: 1-D (1, 1, n),
 // 2-D (1, n0, n1), 3-D (n0, n1, n2); grid axis 0 sits at tile axis zaxis.
+// magic numbers of an unsigned division by d (GenArgs per-level divisors)
+struct GenDiv {
+  uint32_t m, s1, s2;
+};
+__host__ __device__ inline GenDiv gen_div(uint32_t d) {
+  uint32_t l = 0;
+  while ((1u << l) < d) ++l;  // l = ceil(log2 d)
+  GenDiv g;
+  g.m = (uint32_t)((((unsigned long long)1 << 32) * (((unsigned long long)1 << l) - d)) / d) + 1;
+  g.s1 = l > 0 ? 1 : 0;
+  g.s2 = l > 0 ? l - 1 : 0;
+  return g;
+}
+#define EBISU_GEN_MAXT 32  // levels per resident-tile launch
+
 struct GenArgs {
   long long ext[3];
   long long pitch;       // row pitch (elements)
@@ -53,7 +68,9 @@ struct GenArgs {
   int RA[3];             // shrink per level (R on present axes, 0 on absent)
   int F[3];              // frame width per axis
   int nt[3];             // tiles per axis
-  int T;                 // fused levels of this launch
+  int T;                 // fused levels of this launch (<= EBISU_GEN_MAXT)
+  GenDiv lvl_cpr[EBISU_GEN_MAXT];  // level s: row chunks per region row
+  GenDiv lvl_w1[EBISU_GEN_MAXT];   // level s: region rows per plane
   int ntaps;
   int lin[EBISU_MAX_TAPS];  // tile-linear tap offsets
   double coef[EBISU_MAX_TAPS];
