@@ -603,14 +603,15 @@ int run_halo2d_stage(const ProblemDesc& p, const TbKernel* k, int epochs, int fi
         kc = &ks[i];
   }
   int cl = 1, max_ctas = per_sm * di.sms;
-  if (cl_req > 1 && !kc)
-    return fail(EBISU_ERR_UNSUPPORTED,
-                "no cluster-tile halo-exchange kernel for this stencil at depth %d", T);
+  // (no cluster-tile twin for this stencil / depth / arithmetic: the device
+  // tile is one CTA -- the same result, device_tile_grid only shapes the run)
   if (kc) {
     double best = -1;
+    // requested: that many CTAs (portable cluster sizes 1..8); AUTO: 1/2/4/8
+    const int req = std::min(cl_req, 8);
     const int cands[4] = {1, 2, 4, 8};
-    for (int c : cands) {
-      if (cl_req > 0 && c != std::min(cl_req, 8)) continue;
+    for (int i = 0; i < (req > 0 ? 1 : 4); ++i) {
+      const int c = req > 0 ? req : cands[i];
       int slots = per_sm * di.sms;
       if (c > 1) {
         int ncl = 0;

@@ -699,7 +699,7 @@ def test_device_tiles_of_cluster_ctas_bitwise(name, t):
     st = _shape(name)
     r = st.radius
     rng = eb.SplitMix64(0xC1 + 7 * t + len(name))
-    for cl in (2, 4, 8):
+    for cl in ((2, 3, 4, 8) if t == 4 else (2, 4, 8)):
         for n1 in (2 * r + 2, 1024 * cl - 64, 1024 * cl, 2 * 1024 * cl + 4 * r + 38):
             n0 = 2 * r + 1 + rng.randint(0, 200)
             steps = t * rng.randint(1, 2)  # whole epochs: every stage is a halo stage
