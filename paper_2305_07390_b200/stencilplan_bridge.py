@@ -32,6 +32,7 @@ from .grid import Grid as _Grid
 from .grid import sweep as _sweep
 
 _SAVED: dict = {}
+ENGINE_CALLS: dict = {}  # scheme -> B200 engine invocations in this process
 
 
 def _to_params(params):
@@ -63,6 +64,7 @@ def make_engine(sp, scheme: str):
     fn = _engine.ENGINES[scheme]
 
     def b200_engine(grid, stencil, params):
+        ENGINE_CALLS[scheme] = ENGINE_CALLS.get(scheme, 0) + 1
         try:
             p = _to_params(params)
             out, tr = fn(_Grid(grid.cells, grid.boundary), stencil, p)
@@ -130,3 +132,30 @@ def uninstall():
     for (_, name), (mod, value) in list(_SAVED.items()):
         setattr(mod, name, value)
     _SAVED.clear()
+
+
+def main(argv=None) -> int:
+    """``stencilplan`` CLI with the B200 engines -- SURVEY §8(f)4's
+    ``stencilplan simulate --engine b200``:
+
+        python -m paper_2305_07390_b200.stencilplan_bridge simulate --suite s.json
+
+    installs the engines into the unmodified reference package, then hands
+    ``argv`` to the reference's own front end (cli.py:69-123): ``simulate``
+    runs every suite case through ``planner._simulate_one`` on the GPU and
+    checks it against the reference's numpy ``reference_run`` (exit 1 on a
+    mismatch), ``plan`` / ``validate`` / ``report`` / ``catalog`` / ``serve``
+    behave as in the reference (``serve``: HTTP ``POST /simulate`` on the
+    GPU engines)."""
+    import sys
+
+    import stencilplan.cli  # noqa: PLC0415
+
+    install()
+    rc = stencilplan.cli.main(sys.argv[1:] if argv is None else argv)
+    print(f"[b200] engine calls: {sum(ENGINE_CALLS.values())} {ENGINE_CALLS}", file=sys.stderr)
+    return rc
+
+
+if __name__ == "__main__":
+    raise SystemExit(main())

@@ -125,3 +125,32 @@ def test_integration_binding_on_the_reference(tmp_path):
     assert r.returncode == 0, (r.stdout + r.stderr)[-3000:]
     res = json.loads(r.stdout.strip().splitlines()[-1])
     assert res["runs"] == 6 and res["simulated"] == 3
+
+
+def test_cli_simulate_with_b200_engines(tmp_path):
+    """the reference CLI's ``simulate`` on the GPU engines
+    (``python -m paper_2305_07390_b200.stencilplan_bridge simulate``): every
+    suite run goes through planner._simulate_one -> the B200 engine, is
+    checked against the reference's numpy oracle (exit code 0 = all bitwise),
+    and the report lands where the reference writes it."""
+    if not os.path.isdir(os.path.join(REF_PKG, "src")):
+        pytest.skip("baseline/_ref/pkg missing")
+    env = dict(os.environ)
+    env["PYTHONPATH"] = os.pathsep.join([os.path.join(REF_PKG, "src"), ROOT,
+                                         env.get("PYTHONPATH", "")])
+    suite = tmp_path / "suite.json"
+    suite.write_text(json.dumps({
+        "stencils": ["j2d5pt", "j2d9pt-gol", "j3d7pt", "j3d27pt", "j1d3pt"],
+        "domains": {"j2d5pt": [96, 200], "j2d9pt-gol": [64, 130], "j3d7pt": [24, 20, 32],
+                    "j3d27pt": [20, 18, 16], "j1d3pt": [5000]}}))
+    out = tmp_path / "report"
+    cmd = [sys.executable, "-m", "paper_2305_07390_b200.stencilplan_bridge", "simulate",
+           "--suite", str(suite), "--out", str(out), "--workers", "1"]
+    r = subprocess.run(cmd, cwd=ROOT, env=env, capture_output=True, text=True, timeout=900)
+    assert r.returncode == 0, (r.stdout + r.stderr)[-3000:]
+    rep = json.loads((out / "report.json").read_text())
+    runs = rep["runs"]
+    assert rep["ok"] and len(runs) == 5, rep
+    assert all(rec["oracle"] == "pass" for rec in runs), runs[:3]
+    assert "[b200] engine calls: 5 " in r.stderr, r.stderr[-2000:]  # every run on the GPU
+
