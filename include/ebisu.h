@@ -40,7 +40,8 @@
  * ebisu_last_error().  Grids are dense C-order float64 (or, for the _f32
  * entry points, float32) arrays, axis 0 slowest
  * (the streaming axis).  The caller owns every buffer it passes; the library
- * owns only device scratch it allocates itself (released by
+ * owns only device scratch it allocates itself and the pinned host slots it
+ * stages pageable host buffers through (both released by
  * ebisu_release_scratch).  Calls are reentrant; one CUDA stream per call.
  */
 #ifndef EBISU_H
@@ -217,7 +218,8 @@ EBISU_API int32_t ebisu_compare_device(const double* d_a, const double* d_b, int
                              double* max_abs_diff, double* max_abs_ref,
                              void* stream);
 
-/* Free the library's device scratch arena for the current device. */
+/* Free the library's device scratch arena for the current device and the
+ * pinned host slots of the pageable-buffer path. */
 EBISU_API int32_t ebisu_release_scratch(void);
 
 #ifdef __cplusplus

@@ -1454,15 +1454,33 @@ cudaError_t ensure(Pool& P, int K) {
   }
   return cudaSuccess;
 }
-// parallel memcpy of up to K (dst, src, len) jobs
+// parallel memcpy of up to K (dst, src, len) jobs; no exception crosses the
+// C ABI: a job whose thread cannot be created runs on the calling thread
 void par_copy(const std::vector<std::array<size_t, 3>>& jobs) {
+  auto run = [&jobs](size_t i) {
+    memcpy((void*)jobs[i][0], (const void*)jobs[i][1], jobs[i][2]);
+  };
   std::vector<std::thread> th;
-  for (size_t i = 1; i < jobs.size(); ++i)
-    th.emplace_back([&jobs, i] {
-      memcpy((void*)jobs[i][0], (const void*)jobs[i][1], jobs[i][2]);
-    });
-  if (!jobs.empty()) memcpy((void*)jobs[0][0], (const void*)jobs[0][1], jobs[0][2]);
+  for (size_t i = 1; i < jobs.size(); ++i) {
+    try {
+      th.emplace_back(run, i);
+    } catch (...) {
+      run(i);
+    }
+  }
+  if (!jobs.empty()) run(0);
   for (auto& t : th) t.join();
+}
+// free the pinned slots (ebisu_release_scratch)
+void release() {
+  Pool& P = pool();
+  std::lock_guard<std::mutex> lk(P.mu);
+  for (cudaEvent_t ev : P.done) cudaEventSynchronize(ev);
+  for (void* q : P.slots) cudaFreeHost(q);
+  for (cudaEvent_t ev : P.done) cudaEventDestroy(ev);
+  P.slots.clear();
+  P.done.clear();
+  P.dev = -1;
 }
 cudaError_t h2d(void* d, const void* h, size_t bytes, cudaStream_t st) {
   Pool& P = pool();
@@ -1631,6 +1649,7 @@ int32_t ebisu_release_scratch(void) {
   if (cudaGetDevice(&dev) != cudaSuccess) return fail(EBISU_ERR_NO_DEVICE, "no device");
   cudaMemPool_t pool;
   if (cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) cudaMemPoolTrimTo(pool, 0);
+  staging::release();  // pinned host slots of the pageable-buffer path
   return EBISU_OK;
 }
 

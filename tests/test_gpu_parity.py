@@ -758,6 +758,9 @@ def test_host_entry_pageable_and_pinned_buffers_agree():
         assert np.array_equal(inplace, ref), ext
         if ext[0] > 100:  # (the oracle on the 2^28-cell case would take minutes)
             assert np.array_equal(ref, oracle_run(g.cells, taps_of(st), 9))
+        # the pinned slot ring is released and re-created on demand
+        assert lib.ebisu_release_scratch() == 0
+        assert np.array_equal(eb.sweep(g, st, 9, t=4).cells, ref), ext
 
 
 def test_reserve_sms_shrinks_the_persistent_grid():
