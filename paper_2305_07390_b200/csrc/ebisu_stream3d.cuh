@@ -32,6 +32,34 @@
 
 namespace ebisu {
 
+// Tile geometry along one in-plane axis (stream2d_strip's arithmetic for an
+// aligned width, without the frame-column class the 3-D kernels do not use).
+// Kept separate on purpose: the AL-generic 2-D version perturbs ptxas's
+// register allocation of the 3-D kernels (248 vs 254 registers, j3d7pt 512^3
+// 693 vs 733 GCells/s measured A/B on one box).
+__host__ __device__ inline StripGeom tile3d_strip(int j, int ntiles, int aligned, int n, int L,
+                                                  int V, int H) {
+  StripGeom g;
+  g.fc = 0;
+  if (aligned) {
+    const int xl = n - L + H;
+    if (j == ntiles - 1) {
+      g.X0 = n - L;
+      g.vlo = xl;
+      g.vhi = n;
+    } else {
+      g.X0 = j * V;
+      g.vlo = j == 0 ? 0 : j * V + H;
+      g.vhi = min((j + 1) * V + H, xl);
+    }
+  } else {
+    g.X0 = j * V - H;
+    g.vlo = j * V;
+    g.vhi = min((j + 1) * V, n);
+  }
+  return g;
+}
+
 struct Stream3DArgs {
   int n0, n1, n2;   // extents
   int pitch;        // row pitch of every buffer (elements, >= n2); plane pitch n1*pitch
@@ -1059,8 +1087,12 @@ __global__ void __launch_bounds__(NWY * 32, MINB)
       // edge-aligned tiles (a.aligned_x/y): the first tile starts at the
       // domain edge and the last ends there -- the frame needs no halo, so
       // those tiles keep the margin on one side only (fewer tiles per axis)
-      const StripGeom gx = stream2d_strip(tx, a.ntx, a.aligned_x, n2, Cfg::LX, Cfg::VX, Cfg::HX, Cfg::AL);
-      const StripGeom gy = stream2d_strip(ty, a.nty, a.aligned_y, n1, Cfg::LY, Cfg::VY, Cfg::HY);
+      // (x geometry over the 16-byte-aligned width: with an odd, row-padded
+      // last extent the last tile starts on a TMA-aligned column and may store
+      // into the pad column, which is never read)
+      const int n2g = (n2 + Cfg::AL - 1) / Cfg::AL * Cfg::AL;
+      const StripGeom gx = tile3d_strip(tx, a.ntx, a.aligned_x, n2g, Cfg::LX, Cfg::VX, Cfg::HX);
+      const StripGeom gy = tile3d_strip(ty, a.nty, a.aligned_y, n1, Cfg::LY, Cfg::VY, Cfg::HY);
       const int X0 = gx.X0, Y0 = gy.X0;
       const int TR = T * R;
       (void)TR;
