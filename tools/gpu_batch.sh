@@ -1,5 +1,3 @@
 set -x; mkdir -p gpurun_out
-(cd scratch/r01 && timeout 300 python ../../tools/ab3d.py) >> gpurun_out/ab3d4.log 2>&1
-timeout 300 python tools/ab3d.py >> gpurun_out/ab3d4.log 2>&1
-timeout 600 python tools/tune_depths.py j3d7pt j3d27pt j3d17pt poisson j3d13pt >> gpurun_out/ab3d4.log 2>&1
-timeout 900 python -m pytest tests -m gpu -x -q -k "3d or config4 or config5 or odd or reassoc or fp32" > gpurun_out/t3d.log 2>&1; echo "rc=$?" >> gpurun_out/t3d.log
+timeout 900 python bench.py > gpurun_out/f2_bench.json 2> gpurun_out/f2_bench.err
+timeout 900 ncu --set full --clock-control none --import-source on -k regex:k_stream3d -s 1 -c 1 -o gpurun_out/f2_stream3d_j3d7pt_t4 python tools/prof_run.py j3d7pt 512 500 4 > gpurun_out/f2_ncu.log 2>&1
