@@ -446,6 +446,11 @@ def main():
         import torch.distributed as dist
 
         if backend == "nccl":
+            # NCCL's init log (communicator rank count, transports: NVLink P2P /
+            # NVLS) lets the run's log prove every rank joined; INIT only, so
+            # the JSON result line stays the last line rank 0 prints
+            os.environ.setdefault("NCCL_DEBUG", "INFO")
+            os.environ.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
             dist.init_process_group("nccl", device_id=torch.device("cuda", dev))
         else:
             dist.init_process_group(backend)
