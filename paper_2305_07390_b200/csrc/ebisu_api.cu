@@ -251,6 +251,7 @@ enum KernelId : int {
   KID_STREAM3D = 3,
   KID_HALO2D = 4,
   KID_GENERIC = 5,
+  KID_GENERIC_S3D = 6,
 };
 
 // First registered kernel for (shape, depth, exactness) -- the registry lists
@@ -1039,6 +1040,55 @@ int run_generic_stage(const ProblemDesc& p, int T, int epochs, int first_src, in
   return EBISU_OK;
 }
 
+// ---- one-step 3-D streaming for any tap set (k_generic_s3d) -------------------
+// Plan: 128 x 16 output tiles (64-wide when the ring would not fit), z
+// segments so that every resident CTA has units (>= 4 (2R+1) planes each: the
+// 2R-plane prologue is the per-unit overhead); false when no tile fits.
+constexpr int kS3DPrefetch = 1;  // = kGenS3DPrefetch (ebisu_generic.cu)
+constexpr int kS3DTileY = 16;
+bool s3d_plan(const ProblemDesc& p, int sms, GenS3DArgs* a, int* grid, int* smem) {
+  if (p.dims != 3) return false;
+  const int R = p.rad;
+  memset(a, 0, sizeof(*a));
+  a->R = R;
+  a->LY = kS3DTileY;
+  a->LX = 128;
+  auto bytes = [&](int ly, int lx) {  // 2R+1 planes + kS3DPrefetch in flight
+    return (2 * R + 1 + kS3DPrefetch) * (ly + 2 * R) * (lx + 2 * R) * p.elem;
+  };
+  if (bytes(a->LY, a->LX) > kGenSmemBytes) a->LX = 64;
+  if (bytes(a->LY, a->LX) > kGenSmemBytes) return false;
+  *smem = bytes(a->LY, a->LX);
+  a->n0 = p.ext[0];
+  a->n1 = p.ext[1];
+  a->n2 = p.ext[2];
+  a->pitch = p.pitch ? p.pitch : p.ext[2];
+  a->z_lo = p.z_lo;
+  a->z_hi = p.z_hi;
+  a->nty = (int)((p.ext[1] + a->LY - 1) / a->LY);
+  a->ntx = (int)((p.ext[2] + a->LX - 1) / a->LX);
+  const long long tiles = (long long)a->nty * a->ntx;
+  const int per_sm = std::max(1, 228 * 1024 / (*smem + 1024));
+  const long long slots = (long long)sms * std::min(per_sm, 8);
+  const long long span = p.z_hi - p.z_lo;
+  long long nseg = std::max<long long>(1, (2 * slots + tiles - 1) / tiles);
+  const long long min_len = 4LL * (2 * R + 1);
+  nseg = std::min(nseg, std::max<long long>(1, span / min_len));
+  a->seg_len = (int)((span + nseg - 1) / nseg);
+  a->nseg = (int)((span + a->seg_len - 1) / a->seg_len);
+  const long long units = tiles * a->nseg;
+  *grid = (int)std::min<long long>(units, slots);
+  a->ntaps = p.ntaps;
+  const int PX = a->LX + 2 * R;
+  for (int k = 0; k < p.ntaps; ++k) {
+    const int* o = p.offsets + 3 * k;
+    a->dz[k] = o[0];
+    a->lin[k] = o[1] * PX + o[2];
+    a->coef[k] = p.coeffs[k];
+  }
+  return true;
+}
+
 int run_device_impl(const ProblemDesc& p0, const void* d_in, void* d_out, void* d_scr,
                     long long steps, const ebisu_params* prm, cudaStream_t st, Counters* ctr) {
   ProblemDesc p = p0;
@@ -1228,8 +1278,21 @@ int run_device_impl(const ProblemDesc& p0, const void* d_in, void* d_out, void* 
     const int dst = ((nwrites - 1 - w) % 2 == 0) ? BUF_OUT : BUF_SCR;
     if (s.kind == KID_NAIVE) {
       int cs = src, cd = dst;
+      // 3-D steps without a temporal-blocking kernel (user tap sets,
+      // remainders): the streaming one-step kernel unless the naive
+      // yardstick was asked for
+      GenS3DArgs sa;
+      int s3_grid = 0, s3_smem = 0;
+      const bool s3d = scheme != EBISU_SCHEME_NAIVE && s3d_plan(p, di.sms, &sa, &s3_grid, &s3_smem);
       for (int i = 0; i < s.epochs; ++i) {
-        cudaError_t e = launch_naive_step(p, bufs[cs], bufs[cd], exact, st, di.sms);
+        cudaError_t e;
+        if (s3d) {
+          sa.in = bufs[cs];
+          sa.out = bufs[cd];
+          e = launch_generic_s3d(sa, p.elem, exact, s3_grid, s3_smem, st);
+        } else {
+          e = launch_naive_step(p, bufs[cs], bufs[cd], exact, st, di.sms);
+        }
         if (e != cudaSuccess) {
           result = cuda_fail(e, "naive step launch");
           break;
@@ -1243,7 +1306,7 @@ int run_device_impl(const ProblemDesc& p0, const void* d_in, void* d_out, void* 
       ctr->gm_stores += (uint64_t)s.epochs * (uint64_t)total;
       ctr->cells_computed += (uint64_t)s.epochs * (uint64_t)total;
       if (ctr->arith < 0) ctr->arith = exact ? EBISU_ARITH_PER_TAP_EXACT : EBISU_ARITH_PER_TAP_FMA;
-      if (ctr->kid == KID_NONE) ctr->kid = KID_NAIVE;
+      if (ctr->kid == KID_NONE) ctr->kid = s3d ? KID_GENERIC_S3D : KID_NAIVE;
       ctr->t_used = std::max(ctr->t_used, 1);
       src = (s.epochs % 2 == 1) ? dst : (dst == BUF_OUT ? BUF_SCR : BUF_OUT);
     } else if (s.kind == KID_GENERIC) {
@@ -1312,6 +1375,7 @@ const char* ebisu_kernel_name(int32_t id) {
     case KID_STREAM3D: return "stream3d_tb";
     case KID_HALO2D: return "halo2d_tb";
     case KID_GENERIC: return "resident_tb";
+    case KID_GENERIC_S3D: return "stream3d_step";
     default: return "none";
   }
 }

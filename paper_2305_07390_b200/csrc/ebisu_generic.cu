@@ -213,6 +213,165 @@ __global__ void __launch_bounds__(kGenThreads, 1) k_generic_tb(const __grid_cons
   }
 }
 
+// ---- one step, any 3-D tap set: 2.5-D streaming through a plane ring ----------
+// The one-launch-per-step naive kernel reads the z+-R planes of every cell
+// from L2/HBM (512^3 j3d7pt-order-reversed: 180 GCells/s, 0.44 of the naive
+// roofline); here a CTA streams an LY x LX tile along axis 0 and keeps the
+// last 2R+1 planes (with their R-wide ring) in shared memory, so every input
+// cell is loaded once per tile (plus the ring) and every tap is a shared-
+// memory read.  The next plane's cp.async overlaps the current plane's sums.
+constexpr int kGenS3DPrefetch = 1;  // planes in flight (measured: 2 or 3 with 8-row tiles were slower: fewer CTAs per SM)
+
+template <class E, bool EXACT, int NT>
+__global__ void __launch_bounds__(kGenS3DThreads) k_generic_s3d(const __grid_constant__ GenS3DArgs a) {
+  extern __shared__ __align__(16) unsigned char smem[];
+  E* const ring = reinterpret_cast<E*>(smem);
+  const int R = a.R, LY = a.LY, LX = a.LX;
+  const int PY = LY + 2 * R, PX = LX + 2 * R, PL = PY * PX;
+  constexpr int PD = kGenS3DPrefetch;  // planes in flight ahead of the sums
+  const int K = 2 * R + 1 + PD;        // ring slots
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  constexpr int NW = kGenS3DThreads / 32;
+  const long long n0 = a.n0, n1 = a.n1, n2 = a.n2;
+  const E* __restrict__ in = static_cast<const E*>(a.in);
+  E* __restrict__ out = static_cast<E*>(a.out);
+  const int ntaps = NT > 0 ? NT : a.ntaps;
+  const long long units = (long long)a.nty * a.ntx * a.nseg;
+
+  for (long long u = blockIdx.x; u < units; u += gridDim.x) {
+    const int tx = (int)(u % a.ntx);
+    const int ty = (int)((u / a.ntx) % a.nty);
+    const int sg = (int)(u / ((long long)a.ntx * a.nty));
+    const long long Y0 = (long long)ty * LY, X0 = (long long)tx * LX;
+    const long long za = a.z_lo + (long long)sg * a.seg_len;
+    const long long zb = min(a.z_hi, za + a.seg_len);
+    // load plane z (ring slot z mod K), zero outside the domain
+    // in-domain columns of the loaded plane, tile coordinates [clo, chi);
+    // stored columns [0, ohi) and computed (non-frame) ones [clo_f, chi_f)
+    const int clo = (int)max(0LL, (long long)R - X0);
+    const int chi = (int)min((long long)PX, n2 - X0 + R);
+    const int ohi = (int)min((long long)LX, n2 - X0);
+    const int clo_f = (int)max(0LL, (long long)R - X0);
+    const int chi_f = (int)min((long long)LX, n2 - R - X0);
+    auto load = [&](long long z) {
+      E* dst = ring + (int)(((z % K) + K) % K) * PL;
+      const bool zin = z >= 0 && z < n0;
+      for (int r = warp; r < PY; r += NW) {
+        const long long y = Y0 - R + r;
+        const bool yin = zin && y >= 0 && y < n1;
+        // row base at tile column 0 (only dereferenced for in-domain columns)
+        const E* src = in + ((z * n1 + y) * a.pitch + X0 - R);
+        E* d = dst + r * PX;
+        for (int c = lane; c < PX; c += 32) {
+          const bool ok = yin && c >= clo && c < chi;
+          cp_async_zfill(d + c, ok ? src + c : in, ok);
+        }
+      }
+      asm volatile("cp.async.commit_group;" ::: "memory");
+    };
+    // prologue: planes za-R .. za+R-1+PD (one commit group each)
+    for (long long z = za - R; z < za + R + PD; ++z) load(z);
+    for (long long z = za; z < zb; ++z) {
+      // plane z+R is in (at most PD-1 younger groups pending) and every
+      // thread is done with plane z-1, so the slot of plane z-R-1 takes
+      // plane z+R+PD, in flight during the next PD planes' sums
+      asm volatile("cp.async.wait_group %0;" ::"n"(PD - 1) : "memory");
+      __syncthreads();
+      if (z + PD < zb) {
+        load(z + R + PD);
+      } else {
+        asm volatile("cp.async.commit_group;" ::: "memory");  // keep the group count
+      }
+      const bool fz = z < R || z >= n0 - R;
+      const int zs = (int)(z % K);  // ring slot of plane z (z >= 0 here)
+      // ring offset of every tap for this plane (slot of plane z+dz, plus the
+      // in-plane offset): registers when the tap count is a template constant
+      int toff[NT > 0 ? NT : 1];
+      if constexpr (NT > 0) {
+#pragma unroll
+        for (int k = 0; k < NT; ++k) {
+          int slot = zs + a.dz[k];
+          slot += slot < 0 ? K : 0;
+          slot -= slot >= K ? K : 0;
+          toff[k] = slot * PL + a.lin[k];
+        }
+      }
+      for (int r = warp; r < LY; r += NW) {
+        const long long y = Y0 + r;
+        if (y >= n1) break;
+        const bool fy = fz || y < R || y >= n1 - R;
+        const int base = (r + R) * PX + R;
+        E* const orow = out + (z * n1 + y) * a.pitch + X0;
+        for (int c0 = 0; c0 < LX; c0 += 128) {
+          E acc[4];
+          bool live[4], comp[4];
+#pragma unroll
+          for (int j = 0; j < 4; ++j) {
+            const int c = c0 + lane + 32 * j;  // tile column (32-bit tests)
+            live[j] = c < ohi;
+            comp[j] = !fy && c >= clo_f && c < chi_f;
+          }
+          const E* pc = ring + base + c0 + lane;
+          auto tap = [&](int k) -> const E* {
+            if constexpr (NT > 0) {
+              return pc + toff[k];
+            } else {
+              int slot = zs + a.dz[k];
+              slot += slot < 0 ? K : 0;
+              slot -= slot >= K ? K : 0;
+              return pc + slot * PL + a.lin[k];
+            }
+          };
+          {
+            const E* p = tap(0);
+            const E cf = (E)a.coef[0];
+#pragma unroll
+            for (int j = 0; j < 4; ++j) acc[j] = tap_first<EXACT, E>(cf, p[32 * j]);
+          }
+          TapLoop<NT>::run(ntaps, [&](int k) {
+            const E* p = tap(k);
+            const E cf = (E)a.coef[k];
+#pragma unroll
+            for (int j = 0; j < 4; ++j) acc[j] = tap_next<EXACT, E>(acc[j], cf, p[32 * j]);
+          });
+          const E* ctr = ring + zs * PL + base + c0 + lane;
+          E* o = orow + c0 + lane;
+#pragma unroll
+          for (int j = 0; j < 4; ++j)
+            if (live[j]) o[32 * j] = comp[j] ? acc[j] : ctr[32 * j];
+        }
+      }
+    }
+    asm volatile("cp.async.wait_group 0;" ::: "memory");
+    __syncthreads();  // the next unit's prologue overwrites the ring
+  }
+}
+
+template <class E, bool EXACT, int N = 1>
+const void* s3d_kernel_for(int ntaps) {
+  if constexpr (N > kGenMaxNT) {
+    return (const void*)k_generic_s3d<E, EXACT, 0>;
+  } else {
+    if (ntaps == N) return (const void*)k_generic_s3d<E, EXACT, N>;
+    return s3d_kernel_for<E, EXACT, N + 1>(ntaps);
+  }
+}
+
+cudaError_t launch_generic_s3d(const GenS3DArgs& a, int elem, bool exact, int grid, int smem,
+                               cudaStream_t st) {
+  const void* fn;
+  if (elem == 4)
+    fn = exact ? s3d_kernel_for<float, true>(a.ntaps) : s3d_kernel_for<float, false>(a.ntaps);
+  else
+    fn = exact ? s3d_kernel_for<double, true>(a.ntaps) : s3d_kernel_for<double, false>(a.ntaps);
+  cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+  if (e != cudaSuccess) return e;
+  void* args[] = {const_cast<GenS3DArgs*>(&a)};
+  e = cudaLaunchKernel(fn, dim3(grid), dim3(kGenS3DThreads), args, (size_t)smem, st);
+  if (e != cudaSuccess) return e;
+  return cudaGetLastError();
+}
+
 // kernel for (E, EXACT, ntaps): unrolled for 1..kGenMaxNT taps
 template <class E, bool EXACT, int N = 1>
 const void* generic_kernel_for(int ntaps) {

@@ -79,6 +79,26 @@ struct GenArgs {
 };
 cudaError_t launch_generic_tb(const GenArgs& a, int elem, bool exact, int grid, int threads,
                               int smem, cudaStream_t st);
+
+// ---- one-step 2.5-D streaming for any 3-D tap set (ebisu_generic.cu) ----------
+// CTA = LY x LX output tile streamed along axis 0 through a ring of
+// 2R+2 shared-memory planes (each plane loaded once, with its R-wide ring).
+struct GenS3DArgs {
+  long long n0, n1, n2;
+  long long pitch;          // row pitch (elements)
+  long long z_lo, z_hi;     // output planes
+  int R, LY, LX;            // radius, core tile
+  int nty, ntx, nseg, seg_len;
+  int ntaps;
+  int dz[EBISU_MAX_TAPS];   // axis-0 offset of tap k
+  int lin[EBISU_MAX_TAPS];  // in-plane offset dy*(LX+2R) + dx
+  double coef[EBISU_MAX_TAPS];
+  const void* in;
+  void* out;
+};
+cudaError_t launch_generic_s3d(const GenS3DArgs& a, int elem, bool exact, int grid, int smem,
+                               cudaStream_t st);
+constexpr int kGenS3DThreads = 256;
 int generic_threads();
 
 // ---- temporal-blocking kernel registry -------------------------------------

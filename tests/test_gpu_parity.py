@@ -777,3 +777,29 @@ def test_reserve_sms_shrinks_the_persistent_grid():
             t=4, reserve_sms=20), trace=True)
         assert torch.equal(full, part), name
         assert tr1["grid_ctas"] < tr0["grid_ctas"], (name, tr0["grid_ctas"], tr1["grid_ctas"])
+
+
+def test_stream3d_step_kernel_random_user_stencils_bitwise():
+    """3-D tap sets without a temporal-blocking kernel run the one-step
+    streaming kernel (plane ring in shared memory, k_generic_s3d): random
+    user stencils (radius 1-3, random order and coefficients) on ragged and
+    odd grids, exact bitwise, FMA within 1e-12, fp32 within 1e-5; the naive
+    scheme still runs the naive kernel."""
+    rng = eb.SplitMix64(0x53D)
+    for case in range(6):
+        rad = 1 + rng.randint(0, 2)
+        st = _random_shape(rng, 3, rad)
+        ext = tuple(2 * rad + 1 + rng.randint(0, 60) for _ in range(2)) + (
+            2 * rad + 1 + rng.randint(0, 300),)
+        g = eb.random_grid(ext, rng.next_u64())
+        steps = rng.randint(1, 5)
+        ref = oracle_run(g.cells, taps_of(st), steps)
+        out, tr = eb.sweep(g, st, steps, trace=True)
+        assert tr["kernel"] == "stream3d_step", tr
+        assert np.array_equal(out.cells, ref), (case, ext, steps, st.taps)
+        out = eb.sweep(g, st, steps, exact=False)
+        assert np.max(np.abs(out.cells - ref)) <= FMA_RTOL * np.max(np.abs(ref))
+        out = eb.sweep(g, st, steps, dtype=np.float32)
+        assert np.max(np.abs(out.cells - ref)) <= 1e-5 * np.max(np.abs(ref))
+        out, tr = eb.sweep(g, st, steps, scheme=_native.SCHEME_NAIVE, trace=True)
+        assert tr["kernel"] == "naive_step" and np.array_equal(out.cells, ref)
