@@ -819,6 +819,7 @@ int run_tb3d_stage(const ProblemDesc& p, const TbKernel* k, int epochs, int firs
     loads += (uint64_t)n;  // every advance loads one plane (TMA zero-fills past n0)
     adv += (uint64_t)n;
   }
+  ctr->cluster = std::max(ctr->cluster, cl);
   const uint64_t tile_cells = (uint64_t)k->box0 * (uint64_t)k->box1 * (uint64_t)cl;
   ctr->gm_loads += (uint64_t)epochs * loads * tile_cells * (uint64_t)ntx * nty;
   ctr->gm_stores += (uint64_t)epochs * (uint64_t)span * n1 * n2;
@@ -1141,6 +1142,21 @@ int run_device_impl(const ProblemDesc& p0, const void* d_in, void* d_out, void* 
     // overlapped kernels compute the identical result
     if (fam == 1 && best_depth_leq(p.shape_id, D, 64, exact, uni, 1, p.elem) == 0) fam = 0;
     const TbKernel* k = find_tb(p.shape_id, D, t, exact, uni, fam, p.elem, want_c, want_v);
+    // 3-D device tiles of several CTAs (device_tile_grid[0] >= 2 along axis
+    // 1): the 2-CTA cluster tile exchanging its seam rows through DSMEM
+    // (ebisu_stream3d_cl.cuh; engine/device.py:292-389's multi-block streamed
+    // tile), where one is instantiated for this stencil and depth
+    if (D == 3 && scheme == EBISU_SCHEME_DEVICE_TILING && !want_c && !want_v && prm &&
+        prm->device_tile_grid[0] >= 2) {
+      int nk = 0;
+      const TbKernel* ks = tb_kernels(&nk);
+      for (int i = 0; i < nk; ++i)
+        if (ks[i].cluster == 2 && ks[i].shape_id == p.shape_id && ks[i].dims == 3 &&
+            ks[i].T == t && family_ok(ks[i], exact, uni, 0, p.elem)) {
+          k = &ks[i];
+          break;
+        }
+    }
     if (!k && (want_c || want_v))
       return fail(EBISU_ERR_UNSUPPORTED, "no kernel with depth %d, %d cells per lane, variant %d",
                   t, want_c, want_v);

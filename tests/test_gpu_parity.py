@@ -803,3 +803,20 @@ def test_stream3d_step_kernel_random_user_stencils_bitwise():
         assert np.max(np.abs(out.cells - ref)) <= 1e-5 * np.max(np.abs(ref))
         out, tr = eb.sweep(g, st, steps, scheme=_native.SCHEME_NAIVE, trace=True)
         assert tr["kernel"] == "naive_step" and np.array_equal(out.cells, ref)
+
+
+def test_3d_device_tiles_of_two_ctas_bitwise():
+    """run_device_tiling in 3-D with device_tile_grid = (2, 1): the 2-CTA
+    cluster tile (seam rows exchanged through DSMEM every level) where one is
+    instantiated (j3d7pt t = 2, 3), bitwise equal to the oracle; otherwise the
+    one-CTA tile (same result)."""
+    st = _shape("j3d7pt")
+    for t, ext in ((2, (40, 70, 66)), (3, (33, 130, 64)), (4, (20, 40, 36))):
+        g = eb.random_grid(ext, 31 + t)
+        ref = oracle_run(g.cells, taps_of(st), 2 * t)
+        prm = _native.make_params(scheme=_native.SCHEME_DEVICE_TILING, t=t,
+                                  device_tile_grid=(2, 1))
+        out, tr = eb.sweep(g, st, 2 * t, params=prm, trace=True)
+        assert tr["kernel"] == "stream3d_tb", tr
+        assert tr["cluster_ctas"] == (2 if t in (2, 3) else 1), tr
+        assert np.array_equal(out.cells, ref), (t, ext)

@@ -1,3 +1,2 @@
 set -x; mkdir -p gpurun_out
-timeout 1500 python -m pytest tests -m gpu -x -q > gpurun_out/r02_gputest6.log 2>&1; echo "rc=$?" >> gpurun_out/r02_gputest6.log
-timeout 300 python -c "import __graft_entry__ as g; g.smoke()" > gpurun_out/smoke6.log 2>&1; echo "rc=$?" >> gpurun_out/smoke6.log
+timeout 900 python -m pytest tests/test_gpu_parity.py -x -q -k "3d" > gpurun_out/t3dcl.log 2>&1; echo "rc=$?" >> gpurun_out/t3dcl.log
