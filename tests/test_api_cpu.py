@@ -114,3 +114,33 @@ def test_no_cpu_fallback_without_gpu(monkeypatch):
     monkeypatch.setattr(_native, "_lib", None)
     with pytest.raises(_native.NativeUnavailable):
         eb.reference_run(g, st, 3)
+
+
+def test_bridge_cli_runs_the_reference_front_end_without_gpu(tmp_path):
+    """`python -m paper_2305_07390_b200.stencilplan_bridge` hands argv to the
+    unmodified reference CLI after swapping its engines (no GPU work for
+    `catalog`): the wiring the GPU test's `simulate` run relies on."""
+    import os
+    import subprocess
+    import sys
+
+    from conftest import ROOT
+
+    src = None
+    for cand in (os.path.join(ROOT, "baseline", "_ref", "pkg", "src"),
+                 "/root/reference/pkg/src"):
+        if os.path.isdir(os.path.join(cand, "stencilplan")):
+            src = cand
+            break
+    if src is None:
+        import pytest
+
+        pytest.skip("reference package not available")
+    env = dict(os.environ)
+    env["PYTHONPATH"] = os.pathsep.join([src, ROOT, env.get("PYTHONPATH", "")])
+    r = subprocess.run([sys.executable, "-m", "paper_2305_07390_b200.stencilplan_bridge",
+                        "catalog"], cwd=str(tmp_path), env=env, capture_output=True, text=True,
+                       timeout=300)
+    assert r.returncode == 0, r.stderr[-2000:]
+    assert "j2d5pt" in r.stdout and "j3d27pt" in r.stdout
+    assert "[b200] engine calls: 0" in r.stderr
