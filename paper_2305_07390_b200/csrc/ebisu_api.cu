@@ -1482,11 +1482,11 @@ static int32_t run_device_entry(const ebisu_stencil* stencil, int32_t ndim,
 // pageable copies run single-threaded through its own bounce buffer, and a
 // fresh output array takes its page faults inside the D2H copy (measured:
 // 512 MiB H2D 48 ms, D2H 30 ms prefaulted / ~120 ms fresh, vs 10 + 10 ms
-// pinned).  Instead: a process-wide ring of pinned 16 MiB slots; host threads
+// pinned).  Instead: a process-wide ring of pinned slots (256 MiB); host threads
 // copy chunks between the caller's array and the slots (faulting fresh pages
 // in parallel) while the DMA engine moves the previous group of slots.
 namespace staging {
-constexpr size_t kChunk = 16u << 20;
+constexpr size_t kRingBytes = 256u << 20;  // pinned ring: 2K slots of kRingBytes/(2K)
 struct Pool {
   std::mutex mu;  // one staged transfer at a time (concurrent calls queue here)
   std::vector<void*> slots;
@@ -1498,9 +1498,19 @@ Pool& pool() {
   return p;
 }
 int threads() {
-  const unsigned hw = std::thread::hardware_concurrency();
-  return (int)std::max(2u, std::min(8u, hw ? hw / 2 : 2u));
+  static const int n = [] {
+    if (const char* e = getenv("EBISU_STAGING_THREADS")) {  // measurement knob
+      const int v = atoi(e);
+      if (v >= 1 && v <= 64) return v;
+    }
+    // one copy thread per host core, up to 16 (512 MiB each way, fresh
+    // output: 8 threads 87 ms per 8192^2 reference_run call, 16 threads 82)
+    const unsigned hw = std::thread::hardware_concurrency();
+    return (int)std::max(2u, std::min(16u, hw ? hw : 2u));
+  }();
+  return n;
 }
+size_t chunk_bytes() { return kRingBytes / (2 * (size_t)threads()); }
 bool pageable(const void* p) {
   cudaPointerAttributes a;
   if (cudaPointerGetAttributes(&a, p) != cudaSuccess) {
@@ -1524,7 +1534,7 @@ cudaError_t ensure(Pool& P, int K) {
   while ((int)P.slots.size() < 2 * K) {
     void* q = nullptr;
     cudaEvent_t ev;
-    if ((e = cudaMallocHost(&q, kChunk)) != cudaSuccess) return e;
+    if ((e = cudaMallocHost(&q, chunk_bytes())) != cudaSuccess) return e;
     if ((e = cudaEventCreateWithFlags(&ev, cudaEventDisableTiming)) != cudaSuccess) {
       cudaFreeHost(q);
       return e;
@@ -1568,6 +1578,7 @@ cudaError_t h2d(void* d, const void* h, size_t bytes, cudaStream_t st) {
   const int K = threads();
   cudaError_t e = ensure(P, K);
   if (e != cudaSuccess) return e;
+  const size_t kChunk = chunk_bytes();
   const size_t nch = (bytes + kChunk - 1) / kChunk;
   for (size_t g = 0; g < nch; g += K) {
     std::vector<std::array<size_t, 3>> jobs;
@@ -1599,6 +1610,7 @@ cudaError_t d2h(void* h, const void* d, size_t bytes, cudaStream_t st) {
   const int K = threads();
   cudaError_t e = ensure(P, K);
   if (e != cudaSuccess) return e;
+  const size_t kChunk = chunk_bytes();
   const size_t nch = (bytes + kChunk - 1) / kChunk;
   auto issue = [&](size_t g) -> cudaError_t {
     for (size_t c = g; c < std::min(nch, g + K); ++c) {

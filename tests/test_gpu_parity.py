@@ -732,7 +732,7 @@ def test_device_tiles_auto_cluster_full_width():
 def test_host_entry_pageable_and_pinned_buffers_agree():
     """ebisu_run_host stages pageable (numpy) buffers through its pinned slot
     ring with host threads: multi-chunk sizes that are not a multiple of the
-    16 MiB slot, fresh (unfaulted) outputs, aliasing in == out on the host,
+    slot size (8-16 MiB), fresh (unfaulted) outputs, aliasing in == out on the host,
     and pinned buffers (direct DMA) all give the same bitwise result."""
     import ctypes
 
