@@ -1,3 +1,3 @@
 set -x; mkdir -p gpurun_out
-timeout 300 python tools/e2e_breakdown.py > gpurun_out/staging2.log 2>&1
-timeout 900 python -m pytest tests -m gpu -x -q -k "host_entry or concurrent or golden or purity or reference_suite" > gpurun_out/host_tests2.log 2>&1; echo "rc=$?" >> gpurun_out/host_tests2.log
+timeout 300 python -c "import __graft_entry__ as g; g.smoke()" > gpurun_out/f4_smoke.log 2>&1; echo "rc=$?" >> gpurun_out/f4_smoke.log
+timeout 900 python bench.py > gpurun_out/f4_bench.json 2> gpurun_out/f4_bench.err
