@@ -14,11 +14,12 @@
 //    every tiled axis.  Tiles cover the grid (or the output-plane range
 //    [z_lo, z_hi) along axis 0) with their cores; a persistent grid strides
 //    over them.
-//  * The tile lives in shared memory as two ping-pong buffers (up to 227 KB
-//    per SM); level s computes the region shrunk by s*R per side from the
-//    level s-1 buffer.  Taps are tile-linear offsets in the kernel parameter
-//    space (uniform across the warp: constant-bank broadcast); every lane
-//    owns 4 cells of a 128-cell row chunk (4 independent sums in flight).
+//  * The tile lives in shared memory as two ping-pong buffers (2 CTAs x 512
+//    threads x ~113 KB per SM); level s computes the region shrunk by s*R
+//    per side from the level s-1 buffer.  Taps are tile-linear offsets in the
+//    kernel parameter space (uniform across the warp: constant-bank
+//    broadcast; unrolled for up to 27 taps); every lane owns 4 cells of a
+//    128-cell row chunk (4 independent sums in flight).
 //  * Frame cells (distance < R from a face, common.py:96-112) and cells
 //    outside the domain carry their value; a computed interior cell reads only
 //    cells within R, all inside the domain, so the zero-filled outside is
@@ -30,9 +31,13 @@
 //    tolerance mode.
 //  * Per cell-step cost: NT shared loads + 1 shared store (no register
 //    reuse: the pattern is not known at compile time); the host planner
-//    (ebisu_api.cu gen_plan) picks T and the tile shape from that cost and
-//    the HBM round trip, and keeps the one-launch-per-step kernel when it is
-//    cheaper.
+//    (ebisu_api.cu gen_plan) picks the tile shape from that cost and the HBM
+//    round trip.  Measured, it wins over one launch per step in 1-D only, so
+//    AUTO runs 1-D tap sets here (t = 16), 2-D ones on the naive kernel and
+//    3-D ones on k_generic_s3d below (gen_pick_depth).
+//
+// k_generic_s3d: one step of any 3-D tap set, 2.5-D streaming through a
+// shared-memory plane ring (see the kernel's comment).
 #include "ebisu_common.cuh"
 #include "ebisu_internal.h"
 #include "ebisu_shapes.cuh"  // static_for
