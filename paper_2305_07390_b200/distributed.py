@@ -81,18 +81,43 @@ INTERIOR_RESERVE_SMS = 2
 
 
 def _default_step(stencil: StencilShape, exact: bool):
+    """The per-epoch sweep call of the slab driver.  The epoch loop issues three
+    ranged calls per epoch (~0.3 ms of GPU work each at j2d5pt 8192^2 t=8),
+    so the host side is kept lean: the stencil arguments, the extents and the
+    parameter blocks are built once and reused, and the C ABI is called
+    directly on the current stream (same call as device.sweep_device)."""
+    import ctypes
+
     from . import _native, device
+
+    lib = _native.load()
+    sargs = _native.StencilArgs(stencil)
+    ext_cache: dict = {}
+    prm_cache: dict = {}
 
     def step(src, dst, scratch, steps, t, planes=None, frame_ready=False, reserve_sms=0):
         if planes is None:
             device.sweep_device(src, stencil, steps, out=dst, scratch=scratch, t=t, exact=exact)
-        else:
-            # frame_ready: dst already holds the (constant) frame, so the
-            # ranged call skips its frame pre-copy launch; reserve_sms keeps
-            # SMs free of the interior grid for the concurrent NCCL kernels
-            prm = _native.make_params(t=t, exact=exact, out_planes=planes,
-                                      frame_ready=frame_ready, reserve_sms=reserve_sms)
-            device.sweep_device(src, stencil, steps, out=dst, params=prm)
+            return
+        # frame_ready: dst already holds the (constant) frame, so the ranged
+        # call skips its frame pre-copy launch; reserve_sms keeps SMs free of
+        # the interior grid for the concurrent NCCL kernels
+        key = (t, tuple(planes), bool(frame_ready), int(reserve_sms))
+        prm = prm_cache.get(key)
+        if prm is None:
+            prm = prm_cache[key] = _native.make_params(
+                t=t, exact=exact, out_planes=planes, frame_ready=frame_ready,
+                reserve_sms=reserve_sms)
+        shape = tuple(src.shape)
+        ext = ext_cache.get(shape)
+        if ext is None:
+            ext = ext_cache[shape] = _native.extents_c(shape)
+        run = lib.ebisu_run_device_f32 if src.dtype == device._torch().float32 else \
+            lib.ebisu_run_device
+        rc = run(ctypes.byref(sargs.c), src.dim(), ext, src.data_ptr(), dst.data_ptr(), None,
+                 int(steps), ctypes.byref(prm), device._stream_ptr(), None)
+        if rc:
+            raise _native.NativeError(f"libebisu error {rc}: {_native.last_error()}")
 
     return step
 

@@ -1,3 +1,2 @@
 set -x; mkdir -p gpurun_out
-timeout 300 python -c "import __graft_entry__ as g; g.smoke()" > gpurun_out/f4_smoke.log 2>&1; echo "rc=$?" >> gpurun_out/f4_smoke.log
-timeout 900 python bench.py > gpurun_out/f4_bench.json 2> gpurun_out/f4_bench.err
+timeout 900 python -m pytest tests -m gpu -x -q -k "slab or distributed or multi_rank or output_plane or reserve" > gpurun_out/dist_tests.log 2>&1; echo "rc=$?" >> gpurun_out/dist_tests.log
