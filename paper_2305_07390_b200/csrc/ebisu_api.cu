@@ -455,11 +455,18 @@ int run_tb2d_stage(const ProblemDesc& p, const TbKernel* k, int epochs, int firs
   const int span = p.z_hi - p.z_lo;  // output rows of this call
   int nseg = 1, seg_len = span;
   plan_segments(span, nstrips, total_warps, 2 * T * R, std::max(16, 2 * T * R), &nseg, &seg_len);
-  // uniform segments: the guided schedule measured 3 % slower here (per-warp
-  // units are already short; the extra warm-ups cost more than the tail)
+  // Persistent multi-epoch launches: uniform segments (the guided schedule
+  // measured 3 % slower there: dataflow epochs already hide the tail and the
+  // extra warm-ups cost more).  Single-epoch launches (the multi-GPU driver's
+  // per-epoch calls, one launch per epoch) end in a real tail: guided
+  // segments, shortest last.  EBISU_SEG2D=uniform|guided forces one (A/B).
+  const bool multi = coop_req && di.coop && epochs > 1;
+  bool guided = !multi;
+  if (const char* v = getenv("EBISU_SEG2D")) guided = strcmp(v, "guided") == 0;
   const std::vector<int> seg_start =
-      guided_segments(p.z_lo, p.z_hi, nstrips, total_warps, seg_len, seg_len,
-                      seg_rows_req > 0 ? seg_rows_req : seg_len);
+      guided_segments(p.z_lo, p.z_hi, nstrips, total_warps, seg_len,
+                      guided ? std::max(16, 2 * T * R) : seg_len,
+                      seg_rows_req > 0 ? seg_rows_req : (guided ? 0 : seg_len));
   nseg = (int)seg_start.size() - 1;
   const long long units = (long long)nstrips * nseg;
   // every resident warp pulls units dynamically
