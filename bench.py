@@ -532,7 +532,8 @@ def main():
                    "stencil": STENCIL, "extents": [N0, N1], "time_steps": args.tsteps,
                    "fused_depth_t": args.t, "exact": True,
                    "l2": "inputs larger than L2 (512 MiB grid vs 126 MB L2)",
-                   "parallelism": f"slab{world}" if world > 1 else "single"},
+                   "parallelism": f"slab{world}" if world > 1 else "single",
+                   "exchange_every_epochs": runner.exchange_every if world > 1 else None},
         "roofline": {"bound": "hbm", "kernel": "k_stream2d (stream2d_tb)",
                      "achieved": achieved, "peak": hbm_peak, "unit": "GB/s",
                      "frac": achieved / hbm_peak, "traffic": traffic,
@@ -644,7 +645,8 @@ def main():
                 line[key] = {
                     "value": cells3 / (ms3 / 1e3) / 1e9, "unit": "GCells/s", "ms": ms3,
                     "time_steps": 100, "fused_depth_t": 4, "scaling": scaling,
-                    "extents": list(extents), "overlapped_epochs": run3.overlapped_epochs}
+                    "extents": list(extents), "overlapped_epochs": run3.overlapped_epochs,
+                    "exchange_every_epochs": run3.exchange_every}
                 del run3
                 torch.cuda.empty_cache()
             except Exception as exc:  # pragma: no cover - multi-GPU only

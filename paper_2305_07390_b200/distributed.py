@@ -132,7 +132,8 @@ class SlabSweep:
     """
 
     def __init__(self, stencil: StencilShape, extents, t: int, seed: int | None = None,
-                 exact: bool = True, group=None, device=None, step=None, cells=None):
+                 exact: bool = True, group=None, device=None, step=None, cells=None,
+                 exchange_every: int | None = None):
         import torch
         import torch.distributed as dist
 
@@ -143,7 +144,25 @@ class SlabSweep:
         self.group = group
         self.rank = dist.get_rank(group) if dist.is_initialized() else 0
         self.world = dist.get_world_size(group) if dist.is_initialized() else 1
-        self.halo = self.t * stencil.radius
+        # Deep halos: exchange every K epochs with K*t*R ghost planes, the K
+        # epochs in ONE persistent sweep of the whole local slab (ghosts
+        # included): the slab's own frame planes sit in the ghost region, whose
+        # values go stale by R planes per step -- K*t*R planes after K epochs,
+        # exactly the ghost depth -- so the owned planes stay exact, and the
+        # sweep keeps its dataflow epochs (no epoch tail; the per-epoch
+        # band/interior split measured at <= 0.87 of a persistent sweep on one
+        # GPU, tools/slab_split_cost.py).  Cost: 2*K*t*R redundant planes per
+        # rank.  Default: the largest K <= 16 with that redundancy <= 1.6 % of
+        # the owned planes (K = 1: the overlapped per-epoch split).  Measured
+        # on one GPU for a middle rank of config 2 (8192^2 per rank, t=8):
+        # K = 4 / 8 / 16 -> 0.90 / 0.94 / 0.93 of the owned-only sweep, the
+        # per-epoch split 0.86 (profiles/r02_slab_split_cost.txt).
+        R = max(1, stencil.radius)
+        if exchange_every is None:
+            own = self.extents[0] // max(1, self.world)
+            exchange_every = int(0.008 * own // (self.t * R)) if self.world > 1 else 1
+        self.exchange_every = max(1, min(16, int(exchange_every)))
+        self.halo = self.exchange_every * self.t * stencil.radius
         self.plan = slab_plan(self.extents[0], self.world, self.rank, self.halo)
         self.device = device if device is not None else (
             torch.device("cuda", torch.cuda.current_device()) if torch.cuda.is_available()
@@ -319,6 +338,8 @@ class SlabSweep:
         if steps == 0:
             return self.owned()
         own_n = self.plan.own1 - self.plan.own0
+        if self.exchange_every > 1:
+            return self._run_deep(steps)
         split = self.world > 1 and own_n >= 2 * self.halo
         self.exchange(self.halo)  # ghosts current from here on
         done = 0
@@ -337,6 +358,21 @@ class SlabSweep:
                 continue
             self.a, self.b = self.b, self.a
             done += d
+        return self.owned()
+
+    def _run_deep(self, steps: int):
+        """Deep-halo loop: persistent sweeps of K epochs, exchange between."""
+        self.exchange(self.halo)
+        done = 0
+        while done < steps:
+            d = min(self.exchange_every * self.t, steps - done)
+            self.step(self.a, self.b, self.scratch, d, self.t)
+            self.kernel_launches += 3  # TB kernel + frame copies (out, scratch)
+            self._framed.update((self.b.data_ptr(), self.scratch.data_ptr()))
+            self.a, self.b = self.b, self.a
+            done += d
+            if done < steps:
+                self.exchange(self.halo)
         return self.owned()
 
     def gather(self, dst: int = 0):

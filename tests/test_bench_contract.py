@@ -79,4 +79,6 @@ def test_multi_rank_bench_path_on_one_gpu():
     assert d["gpu_launches"] > 0
     for key in ("config5_weak_j3d7pt_1024_per_rank", "config5_strong_j3d7pt_1024_total"):
         c5 = d[key]
-        assert "error" not in c5 and c5["value"] > 0 and c5["overlapped_epochs"] > 0, c5
+        # per-epoch overlapped split, or deep halos (K epochs per exchange)
+        assert "error" not in c5 and c5["value"] > 0, c5
+        assert c5["overlapped_epochs"] > 0 or c5["exchange_every_epochs"] > 1, c5

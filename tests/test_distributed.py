@@ -60,7 +60,8 @@ def _worker(rank, world, port, results):
                 else:
                     dst[planes[0]:planes[1]].copy_(res[planes[0]:planes[1]])
 
-            sw = SlabSweep(st, ext, t=t, seed=1000 + i, step=step, device=torch.device("cpu"))
+            sw = SlabSweep(st, ext, t=t, seed=1000 + i, step=step, device=torch.device("cpu"),
+                           exchange_every=1)
             sw.run(steps)
             own_n = sw.plan.own1 - sw.plan.own0
             if own_n >= 2 * sw.halo and steps >= t:
@@ -68,6 +69,17 @@ def _worker(rank, world, port, results):
             full = sw.gather(0)
             if rank == 0:
                 out[i] = full.numpy()
+            # deep halos: K epochs per exchange, one sweep of the whole local
+            # slab (ghosts included) per K epochs
+            for k in (2, 3):
+                if (ext[0] // world) < 2 * k * t * st.radius:
+                    continue
+                sw = SlabSweep(st, ext, t=t, seed=1000 + i, step=step,
+                               device=torch.device("cpu"), exchange_every=k)
+                sw.run(steps)
+                full = sw.gather(0)
+                if rank == 0:
+                    out[(i, k)] = full.numpy()
         if rank == 0:
             results.update(out)
     finally:
@@ -88,6 +100,10 @@ def test_slab_sweep_matches_oracle(world):
         g = eb.random_grid(ext, 1000 + i)
         ref = reference_run(g.cells, taps_of(st), steps)
         assert np.array_equal(results[i], ref), (world, name, ext, steps, t)
+        for k in (2, 3):
+            if (i, k) in results:
+                assert np.array_equal(results[(i, k)], ref), (world, name, ext, steps, t, k)
+    assert any(isinstance(key, tuple) for key in results.keys())  # deep mode exercised
 
 
 def test_slab_plan_geometry():
@@ -116,12 +132,22 @@ def _gpu_worker(rank, world, port, results):
         out = {}
         for i, (name, ext, steps, t) in enumerate(GPU_CASES):
             st = eb.get_shape(name)
-            sw = SlabSweep(st, ext, t=t, seed=2000 + i, device=torch.device("cuda", 0))
+            sw = SlabSweep(st, ext, t=t, seed=2000 + i, device=torch.device("cuda", 0),
+                           exchange_every=1)
             sw.run(steps)
             torch.cuda.synchronize()
             full = sw.gather(0)
             if rank == 0:
                 out[i] = (full.numpy(), sw.overlapped_epochs)
+            # deep halos (2 epochs per exchange, one persistent sweep each)
+            if ext[0] // world >= 4 * t * st.radius:
+                sw = SlabSweep(st, ext, t=t, seed=2000 + i, device=torch.device("cuda", 0),
+                               exchange_every=2)
+                sw.run(steps)
+                torch.cuda.synchronize()
+                full = sw.gather(0)
+                if rank == 0:
+                    out[(i, 2)] = full.numpy()
         if rank == 0:
             results.update(out)
     finally:
@@ -156,3 +182,6 @@ def test_slab_sweep_gpu_kernels(world):
         got, overlapped = results[i]
         assert np.array_equal(got, ref), (world, name, ext, steps, t)
         assert overlapped == steps // t, (name, overlapped)
+        if (i, 2) in results:
+            assert np.array_equal(results[(i, 2)], ref), (world, name, "deep halo")
+    assert any(isinstance(key, tuple) for key in results.keys())

@@ -47,3 +47,29 @@ print(f"full sweep {full_ms:.2f} ms ({cells / full_ms / 1e6:.0f} GCells/s); "
       f"split reserve 0: {split0_ms:.2f} ms (host {host0:.1f} ms), "
       f"split reserve {INTERIOR_RESERVE_SMS}: {split2_ms:.2f} ms (host {host2:.1f} ms); "
       f"efficiency bound {full_ms / split2_ms:.3f}")
+
+# Deep halos (SlabSweep exchange_every=K): a middle rank sweeps its slab plus
+# K*t*R ghost planes per face in ONE persistent call per K epochs; the
+# exchange would sit between calls.  Efficiency bound vs the plain sweep of
+# the owned rows alone.
+own = torch.empty((n, n), dtype=torch.float64, device="cuda")
+own.copy_(a[H:H + n])
+o2 = torch.empty_like(own); s2 = torch.empty_like(own)
+base_ms, _ = timed(lambda: device.sweep_device(own, st, steps, out=o2, scratch=s2, t=t))
+for K in (4, 8, 16):
+    G = K * t
+    slab = device.random_grid_device((n + 2 * G, n), seed=2)
+    sb = torch.empty_like(slab); ss = torch.empty_like(slab)
+
+    def deep():
+        src, dst = slab, sb
+        done = 0
+        while done < steps:
+            d = min(K * t, steps - done)
+            device.sweep_device(src, st, d, out=dst, scratch=ss, t=t)
+            src, dst = dst, src
+            done += d
+
+    ms, host = timed(deep)
+    print(f"deep halo K={K} (ghost {G} planes/face): {ms:.2f} ms vs owned-only sweep "
+          f"{base_ms:.2f} ms -> efficiency bound {base_ms / ms:.3f}")
